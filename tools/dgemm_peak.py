@@ -1,0 +1,12 @@
+# cuBLAS DGEMM reference throughput (measurement only, never on the solve path)
+import torch, time
+for n in (4096, 8192):
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda"); b = torch.randn_like(a)
+    for _ in range(3): c = a @ b
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10): c = a @ b
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    print(f"DGEMM n={n}: {2*n**3/ms/1e9:.1f} TFLOP/s")
