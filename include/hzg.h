@@ -1,0 +1,110 @@
+/*
+ * hzg.h -- C ABI of libhzg.so, the sm_100a implementation of the blocked
+ * one-sided (implicit) Hari-Zimmermann GSVD hot path.
+ *
+ * Plain pointers and sizes only.  Matrices are split real/imaginary FP64
+ * planes in column-major order, column j of an m-row plane at p + j*m --
+ * exactly the reference's MatrixPlanePair (pkg/src/hzgsvd/core.py:26-69) --
+ * resident in device memory (the caller allocates them, e.g. as torch
+ * tensors, and keeps them alive).  `stream` is a cudaStream_t.
+ *
+ * Each entry point replaces one piece of the reference's CPU driver:
+ *   hzg_create / hzg_bind   -> gsvd_blocked's set-up            (blocked.py:553-572)
+ *   hzg_init_fgz            -> _k_prescale + Z0 = diag(z0)      (blocked.py:564-570, pointwise.py:254-274)
+ *   hzg_sweep               -> one iteration of _algorithm1_loop (blocked.py:521-542),
+ *                              i.e. all outer steps of _block_task (blocked.py:435-484)
+ *                              plus the inter-sweep _k_rescale_full (blocked.py:540-542)
+ *   hzg_finalize            -> final _k_rescale_full (blocked.py:579-581) + _unborder
+ *                              (blocked.py:593-620) + _sort_descending (blocked.py:623-637)
+ *
+ * Return codes mirror the reference's error taxonomy (errors.py:4-23):
+ *   HZG_OK, HZG_RANK -> RankError, HZG_NOT_PD -> NotPositiveDefiniteError,
+ *   HZG_CUDA -> CUDA failure, HZG_INVALID -> ValueError.
+ * Non-convergence is not an error (blocked.py:583-586): the caller counts
+ * sweeps and stops at max_outer_sweeps.
+ */
+#ifndef HZG_H_
+#define HZG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { HZG_OK = 0, HZG_RANK = 1, HZG_NOT_PD = 2, HZG_CUDA = 3, HZG_INVALID = 4 };
+
+/* SolverConfig (pointwise.py:40-81), decoded fields */
+typedef struct {
+  int32_t variant_id;       /* 0..7 */
+  int32_t outer_mm;         /* outer_kind == "mm" */
+  int32_t inner_mm;         /* inner_kind == "mm" */
+  int32_t max_inner_sweeps; /* 30 for blocking "fb", 1 for "bo" (already decoded) */
+  int32_t max_outer_sweeps; /* 30 */
+  int32_t block_width;      /* w; the pair is bordered to multiples of 2w */
+  int32_t sorting;
+  int32_t fallback_qr;
+  int32_t shorten_qr;       /* shorten == "qr" */
+  double gate_eps;          /* 2**-52 */
+  int32_t exact;            /* 1: reference-order Grammian / postmultiply kernels */
+} hzg_config;
+
+typedef struct hzg_ctx hzg_ctx;
+
+/* Problem of bordered size mF x n, mG x n (n and both heights multiples of
+ * 2w).  epsn <= 0 selects gate_eps * sqrt(n) (blocked.py:571-572). */
+int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int32_t is_complex,
+               const hzg_config* cfg, double epsn);
+
+/* Bytes of device workspace hzg_bind needs. */
+size_t hzg_workspace_bytes(const hzg_ctx* ctx);
+
+/* Attach the device planes (F mF x n, G mG x n, Z n x n; imaginary planes
+ * NULL for real problems), a workspace of hzg_workspace_bytes() bytes and
+ * the stream all work is ordered on. */
+int hzg_bind(hzg_ctx* ctx, double* Fr, double* Fi, double* Gr, double* Gi, double* Zr, double* Zi,
+             void* workspace, void* stream);
+
+/* Replace the per-step block-pair schedule: colpairs[step][k] = (c0, c1),
+ * the physical column offsets of pair k of the step (block with the smaller
+ * logical index first).  Used to run a slot range of the ordering on one
+ * GPU of a multi-GPU job.  npairs <= n / (2w). */
+int hzg_set_schedule(hzg_ctx* ctx, const int32_t* colpairs, int32_t osteps, int32_t npairs);
+
+/* Initial G column scaling and Z0 (synchronous: returns the status). */
+int hzg_init_fgz(hzg_ctx* ctx);
+
+/* One outer sweep; returns the sweep's transform counters.  The inter-sweep
+ * Z rescale runs on the device when big != 0.  Synchronous. */
+int hzg_sweep(hzg_ctx* ctx, int64_t* total, int64_t* big);
+
+/* Run outer steps [first, first + count) of the schedule without the sweep
+ * bookkeeping (asynchronous; for profiling and bounded benchmarks). */
+int hzg_run_steps(hzg_ctx* ctx, int32_t first, int32_t count);
+
+/* Final rescale, unborder to n0 columns (mF0 / mG0 rows) and stable
+ * descending sort by sigma (sort = 0 keeps the column order, as
+ * gsvd_blocked does), into caller-provided device outputs: U (mF0 x
+ * n0), V (mG0 x n0), Z (n0 x n0) planes and three length-n0 vectors.
+ * Synchronous. */
+int hzg_finalize(hzg_ctx* ctx, int64_t n0, int64_t mF0, int64_t mG0, int32_t sort, double* Ur, double* Ui,
+                 double* Vr, double* Vi, double* Zr, double* Zi, double* sigF, double* sigG, double* sig);
+
+/* Kernel-level check entry: run the inner block kernel (Cholesky + in-block
+ * prescale + pointwise sweeps + theta rescale) on one block pair given its
+ * two tw x tw Grammians in host memory (column-major planes; imaginary
+ * planes ignored for real).  Outputs Z~ (host, planes) and counters
+ * {total, big, status, inner sweeps}.  Synchronous. */
+int hzg_test_block(int32_t tw, int32_t is_complex, const hzg_config* cfg, double epsn, const double* gFr,
+                   const double* gFi, const double* gGr, const double* gGi, double* zr, double* zi,
+                   int32_t* counts4);
+
+const char* hzg_last_error(const hzg_ctx* ctx);
+void hzg_destroy(hzg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HZG_H_ */

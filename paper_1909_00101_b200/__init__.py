@@ -1,0 +1,26 @@
+"""B200-native blocked one-sided (implicit) Hari-Zimmermann GSVD.
+
+Drop-in for the reference package's GSVD entry point (hzgsvd.solve,
+pkg/src/hzgsvd/blocked.py:640-663): same inputs, same GsvdResult, same
+configuration and exceptions, with the hot path in hand-written sm_100a
+CUDA (libhzg.so, C ABI in include/hzg.h).
+"""
+
+from .config import EPS, SolverConfig, SweepStats
+from .core import (GsvdResult, MatrixPlanePair, ProblemPair, border_pair, read_matrix,
+                   write_matrix)
+from .errors import (DeviceError, FileFormatError, HzgsvdError, NotPositiveDefiniteError,
+                     ProtocolError, RankError)
+from .solver import DeviceGsvd, gsvd_1x1, gsvd_blocked, solve, upload_bordered
+from .strategies import (CommMapping, StrategyTable, block_moves, circle_positions, comm_mapping,
+                         dump_table, gen_table, validate_table)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "EPS", "SolverConfig", "SweepStats", "GsvdResult", "MatrixPlanePair", "ProblemPair", "border_pair",
+    "read_matrix", "write_matrix", "DeviceError", "FileFormatError", "HzgsvdError",
+    "NotPositiveDefiniteError", "ProtocolError", "RankError", "DeviceGsvd", "gsvd_1x1", "gsvd_blocked",
+    "solve", "upload_bordered", "CommMapping", "StrategyTable", "block_moves", "circle_positions",
+    "comm_mapping", "dump_table", "gen_table", "validate_table",
+]

@@ -1,0 +1,96 @@
+"""ctypes binding of libhzg.so (the C ABI declared in include/hzg.h).
+
+There is no fallback: if the library is missing or no CUDA device is
+present, every entry point raises DeviceError.
+"""
+
+import ctypes
+import os
+import threading
+
+from .errors import DeviceError, NotPositiveDefiniteError, RankError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libhzg.so")
+
+HZG_OK, HZG_RANK, HZG_NOT_PD, HZG_CUDA, HZG_INVALID = 0, 1, 2, 3, 4
+
+
+class HzgConfig(ctypes.Structure):
+    _fields_ = [("variant_id", ctypes.c_int32), ("outer_mm", ctypes.c_int32), ("inner_mm", ctypes.c_int32),
+                ("max_inner_sweeps", ctypes.c_int32), ("max_outer_sweeps", ctypes.c_int32),
+                ("block_width", ctypes.c_int32), ("sorting", ctypes.c_int32), ("fallback_qr", ctypes.c_int32),
+                ("shorten_qr", ctypes.c_int32), ("gate_eps", ctypes.c_double), ("exact", ctypes.c_int32)]
+
+
+EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_init_fgz", "hzg_sweep",
+           "hzg_run_steps", "hzg_finalize", "hzg_test_block", "hzg_last_error", "hzg_destroy")
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path=LIB_PATH):
+    """Load libhzg.so and declare its signatures (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise DeviceError("libhzg.so not built (%s); run __graft_entry__.build()" % path)
+        L = ctypes.CDLL(path)
+        P, I32, I64, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        L.hzg_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, I64, I64, I64, I32,
+                                 ctypes.POINTER(HzgConfig), D]
+        L.hzg_create.restype = ctypes.c_int
+        L.hzg_workspace_bytes.argtypes = [P]
+        L.hzg_workspace_bytes.restype = ctypes.c_size_t
+        L.hzg_bind.argtypes = [P] + [P] * 6 + [P, P]
+        L.hzg_bind.restype = ctypes.c_int
+        L.hzg_set_schedule.argtypes = [P, P, I32, I32]
+        L.hzg_set_schedule.restype = ctypes.c_int
+        L.hzg_init_fgz.argtypes = [P]
+        L.hzg_init_fgz.restype = ctypes.c_int
+        L.hzg_sweep.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.hzg_sweep.restype = ctypes.c_int
+        L.hzg_run_steps.argtypes = [P, I32, I32]
+        L.hzg_run_steps.restype = ctypes.c_int
+        L.hzg_finalize.argtypes = [P, I64, I64, I64] + [P] * 9
+        L.hzg_finalize.restype = ctypes.c_int
+        L.hzg_test_block.argtypes = [I32, I32, ctypes.POINTER(HzgConfig), D] + [P] * 6 + [P]
+        L.hzg_test_block.restype = ctypes.c_int
+        L.hzg_last_error.argtypes = [P]
+        L.hzg_last_error.restype = ctypes.c_char_p
+        L.hzg_destroy.argtypes = [P]
+        L.hzg_destroy.restype = None
+        _lib = L
+        return L
+
+
+def make_config(cfg):
+    """Decode a SolverConfig into the C struct."""
+    return HzgConfig(cfg.variant_id, int(cfg.outer_kind == "mm"), int(cfg.inner_kind == "mm"),
+                     cfg.max_inner_sweeps, cfg.max_outer_sweeps, cfg.block_width, int(bool(cfg.sorting)),
+                     int(bool(cfg.fallback_qr)), int(cfg.shorten == "qr"), float(cfg.gate_eps),
+                     int(bool(getattr(cfg, "exact", False))))
+
+
+def check(code, ctx=None, what=""):
+    """Map a C status to the reference's exceptions."""
+    if code == HZG_OK:
+        return
+    msg = what
+    if ctx is not None:
+        try:
+            m = load().hzg_last_error(ctx)
+            if m:
+                msg = "%s: %s" % (what, m.decode()) if what else m.decode()
+        except Exception:
+            pass
+    if code == HZG_NOT_PD:
+        raise NotPositiveDefiniteError(msg)
+    if code == HZG_RANK:
+        raise RankError(msg)
+    if code == HZG_INVALID:
+        raise ValueError(msg or "invalid argument to the device solver")
+    raise DeviceError(msg or "CUDA failure")

@@ -1,0 +1,491 @@
+// C ABI and host-side sweep driver of libhzg.so (see include/hzg.h).
+//
+// One outer sweep = for every step of the outer strategy table: Grammian
+// partials -> inner block kernel -> postmultiply, then the counter fold and
+// the (device-gated) inter-sweep rescale.  The whole sweep is captured once
+// into a CUDA graph and replayed; the host syncs once per sweep to read
+// the two counters the reference's convergence test needs
+// (blocked.py:531-539).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hzg.h"
+#include "hzg_internal.h"
+
+using namespace hzg;
+
+struct hzg_ctx {
+  int device = 0;
+  int64_t mF = 0, mG = 0, n = 0;
+  int cplx = 0;
+  hzg_config cfg{};
+  double epsn = 0;
+  int w = 0, tw = 0, nblk = 0;
+  int osteps = 0, npairs = 0, isteps = 0;
+  bool use_dmma = false;
+  std::vector<int32_t> colpair_host;  // [osteps][npairs][2]
+  std::vector<int32_t> itable_host;   // [isteps][tw]
+  // device state
+  Plane F{}, G{}, Z{};
+  cudaStream_t stream = nullptr;
+  cudaStream_t cap = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  unsigned char* ws = nullptr;
+  int32_t* d_colpair = nullptr;
+  int32_t* d_itable = nullptr;
+  GramWS gw{};
+  InnerOut io{};
+  int64_t* d_ctr = nullptr;    // 4 int64: total, big, status, pad
+  int32_t* d_status = nullptr; // init/final status
+  double* d_qr = nullptr;
+  int32_t* d_qrlock = nullptr;
+  int qr_slots = 0;
+  int32_t* d_fin = nullptr;    // 2n int32
+  double* d_sig = nullptr;     // 3n
+  int64_t* h_ctr = nullptr;    // pinned
+  std::string err;
+  bool bound = false;
+};
+
+namespace {
+
+// strategies.py:45-93 (the same tables the Python layer exposes)
+int gen_table(bool mm, int n, std::vector<int32_t>& out) {
+  const int half = n / 2;
+  out.assign((size_t)n * half * 2, 0);
+  auto sort_row = [&](int st) {
+    std::vector<std::pair<int, int>> v(half);
+    for (int i = 0; i < half; ++i) v[i] = {out[((size_t)st * half + i) * 2], out[((size_t)st * half + i) * 2 + 1]};
+    std::sort(v.begin(), v.end());
+    for (int i = 0; i < half; ++i) {
+      out[((size_t)st * half + i) * 2] = v[i].first;
+      out[((size_t)st * half + i) * 2 + 1] = v[i].second;
+    }
+  };
+  if (!mm) {  // round-robin tournament, strategies.py:59-70
+    std::vector<int> others(n - 1);
+    for (int i = 1; i < n; ++i) others[i - 1] = i;
+    for (int st = 0; st < n - 1; ++st) {
+      std::vector<int> line(n);
+      line[0] = 0;
+      for (int i = 1; i < n; ++i) line[i] = others[i - 1];
+      for (int i = 0; i < half; ++i) {
+        int a = line[i], b = line[n - 1 - i];
+        out[((size_t)st * half + i) * 2] = std::min(a, b);
+        out[((size_t)st * half + i) * 2 + 1] = std::max(a, b);
+      }
+      sort_row(st);
+      std::rotate(others.rbegin(), others.rbegin() + 1, others.rend());
+    }
+    return n - 1;
+  }
+  // modified modulus, strategies.py:73-93
+  for (int k = 0; k < n; ++k) {
+    std::vector<char> seen(n, 0);
+    int cnt = 0;
+    for (int i = 0; i < n; ++i) {
+      if (seen[i]) continue;
+      int j = ((k - i) % n + n) % n;
+      if (j == i || seen[j]) continue;
+      seen[i] = seen[j] = 1;
+      out[((size_t)k * half + cnt) * 2] = std::min(i, j);
+      out[((size_t)k * half + cnt) * 2 + 1] = std::max(i, j);
+      ++cnt;
+    }
+    if (k % 2 == 0) {
+      int a = k / 2, b = a + half;
+      if (!seen[a]) {
+        out[((size_t)k * half + cnt) * 2] = std::min(a, b);
+        out[((size_t)k * half + cnt) * 2 + 1] = std::max(a, b);
+        ++cnt;
+      }
+    }
+    sort_row(k);
+  }
+  return n;
+}
+
+int64_t pow2c(int64_t v) {
+  int64_t m = 1;
+  while (m < v) m <<= 1;
+  return m;
+}
+
+size_t al(size_t v) { return (v + 255) & ~(size_t)255; }
+
+int fail(hzg_ctx* c, int code, const char* what) {
+  if (c) c->err = what;
+  return code;
+}
+
+int cuda_fail(hzg_ctx* c, cudaError_t e, const char* where) {
+  if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+  return HZG_CUDA;
+}
+
+// Grammian split geometry per matrix height (depends on m only, never on
+// the GPU count, so results are GPU-count invariant).
+void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
+  if (exact) {
+    int64_t P = pow2c(m);
+    chunk = std::max<int64_t>(32, std::min<int64_t>(P, 2048));
+    nsplit = (int)std::max<int64_t>(1, P / chunk);
+  } else {
+    chunk = 1024;
+    nsplit = (int)pow2c((m + chunk - 1) / chunk);
+  }
+}
+
+struct Layout {
+  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, total;
+};
+
+Layout layout(const hzg_ctx* c) {
+  Layout L{};
+  const int NP = c->cplx ? 2 : 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += al(bytes);
+    return o;
+  };
+  L.colpair = take((size_t)c->osteps * c->npairs * 2 * 4);
+  L.itable = take((size_t)c->isteps * c->tw * 4);
+  L.part = take((size_t)c->npairs * 2 * c->gw.smax * NP * c->tw * c->tw * 8);
+  L.zt = take((size_t)c->npairs * NP * c->tw * c->tw * 8);
+  L.ident = take((size_t)c->npairs * 4);
+  L.counts = take((size_t)c->osteps * c->npairs * 4 * 4);
+  L.ctr = take(4 * 8);
+  L.status = take(4 * 4);
+  int64_t mmax = std::max(c->mF, c->mG);
+  L.qr = take((size_t)c->qr_slots * 2 * mmax * c->tw * 8);
+  L.qrlock = take((size_t)c->qr_slots * 4);
+  L.fin = take((size_t)2 * c->n * 4);
+  L.sig = take((size_t)3 * c->n * 8);
+  L.total = off;
+  return L;
+}
+
+KernelCfg kernel_cfg(const hzg_ctx* c) {
+  KernelCfg k{};
+  const int v = c->cfg.variant_id;
+  k.tw = c->tw;
+  k.cplx = c->cplx;
+  k.prescale = (v == 0 || v == 1 || v == 4 || v == 5);
+  k.per_step_rescale = !k.prescale;
+  k.compensated = v % 2 == 1;
+  k.crit_c2 = v >= 4;
+  k.sorting = c->cfg.sorting;
+  k.max_inner_sweeps = c->cfg.max_inner_sweeps;
+  k.fallback_qr = c->cfg.fallback_qr;
+  k.epsn = c->epsn;
+  return k;
+}
+
+int launch_step(hzg_ctx* c, int step, cudaStream_t s) {
+  StepPairs sp{c->d_colpair, c->npairs};
+  KernelCfg kc = kernel_cfg(c);
+  int rc = c->use_dmma ? launch_gram_dmma(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s)
+                       : launch_gram_exact(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s);
+  if (rc) return rc;
+  rc = launch_inner(c->F, c->G, sp, step, kc, c->gw, c->d_itable, c->isteps, c->io, c->d_qr, c->qr_slots,
+                    c->d_qrlock, s);
+  if (rc) return rc;
+  return c->use_dmma ? launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s)
+                     : launch_postmult_exact(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s);
+}
+
+int status_code(int64_t st) {
+  if (st & ST_NOT_PD) return HZG_NOT_PD;
+  if (st & (ST_RANK | ST_QR_RANK)) return HZG_RANK;
+  return HZG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int32_t is_complex,
+               const hzg_config* cfg, double epsn) {
+  if (!out || !cfg) return HZG_INVALID;
+  *out = nullptr;
+  const int w = cfg->block_width;
+  if (w < 1 || n < 2 * w || n % (2 * w) != 0 || mF % (2 * w) != 0 || mG % (2 * w) != 0 || mF < 1 || mG < 1)
+    return HZG_INVALID;
+  if (cfg->variant_id < 0 || cfg->variant_id > 7) return HZG_INVALID;
+  if (cfg->variant_id % 2 == 1) return HZG_INVALID;  // compensated dots: not on the device path yet
+  if (cfg->shorten_qr) return HZG_INVALID;           // shorten="qr": not on the device path yet
+  if (2 * w > 64 || (2 * w > 32 && 2 * w != 48 && 2 * w != 64)) return HZG_INVALID;
+  static const int supported[] = {2, 4, 6, 8, 10, 12, 14, 16, 20, 24, 32, 48, 64};
+  bool ok = false;
+  for (int t : supported) ok |= (t == 2 * w);
+  if (!ok) return HZG_INVALID;
+  if (n / w > 65534) return HZG_INVALID;
+  hzg_ctx* c = new hzg_ctx();
+  c->device = device;
+  c->mF = mF;
+  c->mG = mG;
+  c->n = n;
+  c->cplx = is_complex ? 1 : 0;
+  c->cfg = *cfg;
+  if (c->cfg.max_inner_sweeps <= 0) c->cfg.max_inner_sweeps = 30;
+  c->epsn = epsn > 0 ? epsn : cfg->gate_eps * std::sqrt((double)n);
+  c->w = w;
+  c->tw = 2 * w;
+  c->nblk = (int)(n / w);
+  c->npairs = c->nblk / 2;
+  c->use_dmma = !cfg->exact && dmma_supported(w);
+  std::vector<int32_t> outer;
+  c->osteps = gen_table(cfg->outer_mm != 0, c->nblk, outer);
+  c->colpair_host.resize((size_t)c->osteps * c->npairs * 2);
+  for (size_t e = 0; e < c->colpair_host.size(); ++e) c->colpair_host[e] = outer[e] * w;
+  std::vector<int32_t> inner;
+  c->isteps = gen_table(cfg->inner_mm != 0, c->tw, inner);
+  c->itable_host.assign(inner.begin(), inner.begin() + (size_t)c->isteps * c->tw);
+  for (int mat = 0; mat < 2; ++mat) gram_split(mat == 0 ? mF : mG, !c->use_dmma, c->gw.nsplit[mat], c->gw.chunk[mat]);
+  c->gw.smax = std::max(c->gw.nsplit[0], c->gw.nsplit[1]);
+  c->qr_slots = (int)std::max<int64_t>(1, std::min<int64_t>(16, c->npairs));
+  *out = c;
+  return HZG_OK;
+}
+
+size_t hzg_workspace_bytes(const hzg_ctx* c) { return c ? layout(c).total : 0; }
+
+int hzg_set_schedule(hzg_ctx* c, const int32_t* colpairs, int32_t osteps, int32_t npairs) {
+  if (!c || !colpairs || osteps < 1 || npairs < 1 || npairs > c->nblk / 2) return HZG_INVALID;
+  if (c->bound) return fail(c, HZG_INVALID, "hzg_set_schedule must precede hzg_bind");
+  c->osteps = osteps;
+  c->npairs = npairs;
+  c->colpair_host.assign(colpairs, colpairs + (size_t)osteps * npairs * 2);
+  c->qr_slots = std::max(1, std::min(16, npairs));
+  return HZG_OK;
+}
+
+int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double* Zr, double* Zi, void* workspace,
+             void* stream) {
+  if (!c || !Fr || !Gr || !Zr || !workspace) return HZG_INVALID;
+  if (c->cplx && (!Fi || !Gi || !Zi)) return fail(c, HZG_INVALID, "complex problem needs imaginary planes");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+  c->F = Plane{Fr, c->cplx ? Fi : nullptr, c->mF, c->mF};
+  c->G = Plane{Gr, c->cplx ? Gi : nullptr, c->mG, c->mG};
+  c->Z = Plane{Zr, c->cplx ? Zi : nullptr, c->n, c->n};
+  c->stream = (cudaStream_t)stream;
+  Layout L = layout(c);
+  c->ws = (unsigned char*)workspace;
+  c->d_colpair = (int32_t*)(c->ws + L.colpair);
+  c->d_itable = (int32_t*)(c->ws + L.itable);
+  c->gw.part = (double*)(c->ws + L.part);
+  c->io.zt = (double*)(c->ws + L.zt);
+  c->io.ident = (int32_t*)(c->ws + L.ident);
+  c->io.counts = (int32_t*)(c->ws + L.counts);
+  c->d_ctr = (int64_t*)(c->ws + L.ctr);
+  c->d_status = (int32_t*)(c->ws + L.status);
+  c->d_qr = (double*)(c->ws + L.qr);
+  c->d_qrlock = (int32_t*)(c->ws + L.qrlock);
+  c->d_fin = (int32_t*)(c->ws + L.fin);
+  c->d_sig = (double*)(c->ws + L.sig);
+  if ((e = cudaMemcpyAsync(c->d_colpair, c->colpair_host.data(), c->colpair_host.size() * 4,
+                           cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "upload schedule");
+  if ((e = cudaMemcpyAsync(c->d_itable, c->itable_host.data(), c->itable_host.size() * 4, cudaMemcpyHostToDevice,
+                           c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "upload inner table");
+  cudaMemsetAsync(c->d_qrlock, 0, (size_t)c->qr_slots * 4, c->stream);
+  cudaMemsetAsync(c->io.counts, 0, (size_t)c->osteps * c->npairs * 16, c->stream);
+  if (!c->h_ctr) {
+    if ((e = cudaMallocHost(&c->h_ctr, 8 * 8)) != cudaSuccess) return cuda_fail(c, e, "cudaMallocHost");
+  }
+  if (!c->cap) {
+    if ((e = cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(c, e, "cudaStreamCreate");
+  }
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "bind sync");
+  if (c->gexec) {
+    cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+  }
+  if (c->graph) {
+    cudaGraphDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  c->bound = true;
+  return HZG_OK;
+}
+
+int hzg_init_fgz(hzg_ctx* c) {
+  if (!c || !c->bound) return HZG_INVALID;
+  cudaError_t e;
+  const size_t zb = (size_t)c->n * c->n * 8;
+  cudaMemsetAsync(c->Z.re, 0, zb, c->stream);
+  if (c->Z.im) cudaMemsetAsync(c->Z.im, 0, zb, c->stream);
+  cudaMemsetAsync(c->d_status, 0, 16, c->stream);
+  KernelCfg kc = kernel_cfg(c);
+  int rc = launch_prescale(c->F, c->G, c->Z, c->n, c->cplx, kc.prescale, c->d_status, c->stream);
+  if (rc) return fail(c, rc, "prescale launch");
+  int32_t st = 0;
+  if ((e = cudaMemcpyAsync(c->h_ctr, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "status copy");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "prescale");
+  std::memcpy(&st, c->h_ctr, 4);
+  if (st) return fail(c, HZG_RANK, "zero G column during prescaling");
+  return HZG_OK;
+}
+
+static int build_graph(hzg_ctx* c) {
+  cudaError_t e;
+  if ((e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+    return cuda_fail(c, e, "begin capture");
+  int rc = HZG_OK;
+  for (int st = 0; st < c->osteps && rc == HZG_OK; ++st) rc = launch_step(c, st, c->cap);
+  if (rc == HZG_OK) rc = launch_counters(c->io.counts, (int64_t)c->osteps * c->npairs, c->d_ctr, c->cap);
+  if (rc == HZG_OK)
+    rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 0, nullptr, nullptr, nullptr, c->d_ctr, c->d_status,
+                        c->cap);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(c->cap, &g);
+  if (rc != HZG_OK) {
+    if (g) cudaGraphDestroy(g);
+    return fail(c, rc, "kernel launch during capture");
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "end capture");
+  c->graph = g;
+  if ((e = cudaGraphInstantiate(&c->gexec, g, 0)) != cudaSuccess) return cuda_fail(c, e, "graph instantiate");
+  return HZG_OK;
+}
+
+int hzg_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
+  if (!c || !c->bound) return HZG_INVALID;
+  cudaError_t e;
+  if (!c->gexec) {
+    int rc = build_graph(c);
+    if (rc) return rc;
+  }
+  if ((e = cudaGraphLaunch(c->gexec, c->stream)) != cudaSuccess) return cuda_fail(c, e, "graph launch");
+  if ((e = cudaMemcpyAsync(c->h_ctr, c->d_ctr, 3 * 8, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "counter copy");
+  if ((e = cudaMemcpyAsync(c->h_ctr + 3, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "status copy");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "sweep");
+  if (total) *total = c->h_ctr[0];
+  if (big) *big = c->h_ctr[1];
+  int rc = status_code(c->h_ctr[2]);
+  if (rc == HZG_NOT_PD) return fail(c, rc, "indefinite block Grammian; enable the QR fallback");
+  if (rc == HZG_RANK) return fail(c, rc, "rank-deficient block pair in the inner solve");
+  int32_t st = 0;
+  std::memcpy(&st, c->h_ctr + 3, 4);
+  if (st) return fail(c, HZG_RANK, "zero pencil column between sweeps");
+  return HZG_OK;
+}
+
+int hzg_run_steps(hzg_ctx* c, int32_t first, int32_t count) {
+  if (!c || !c->bound || first < 0 || first + count > c->osteps) return HZG_INVALID;
+  for (int s = first; s < first + count; ++s) {
+    int rc = launch_step(c, s, c->stream);
+    if (rc) return fail(c, rc, "step launch");
+  }
+  return HZG_OK;
+}
+
+int hzg_finalize(hzg_ctx* c, int64_t n0, int64_t mF0, int64_t mG0, int32_t sort, double* Ur, double* Ui, double* Vr,
+                 double* Vi, double* Zr, double* Zi, double* sigF, double* sigG, double* sig) {
+  if (!c || !c->bound || n0 < 1 || n0 > c->n || mF0 > c->mF || mG0 > c->mG) return HZG_INVALID;
+  cudaError_t e;
+  double* sF = c->d_sig;
+  double* sG = sF + c->n;
+  double* s = sG + c->n;
+  cudaMemsetAsync(c->d_status, 0, 16, c->stream);
+  int rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 1, sF, sG, s, nullptr, c->d_status, c->stream);
+  if (rc) return fail(c, rc, "final rescale launch");
+  if ((e = cudaMemcpyAsync(c->h_ctr, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "status copy");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "final rescale");
+  int32_t st = 0;
+  std::memcpy(&st, c->h_ctr, 4);
+  if (st) return fail(c, HZG_RANK, "zero column at extraction");
+  Plane Uo{Ur, c->cplx ? Ui : nullptr, mF0, mF0};
+  Plane Vo{Vr, c->cplx ? Vi : nullptr, mG0, mG0};
+  Plane Zo{Zr, c->cplx ? Zi : nullptr, n0, n0};
+  rc = launch_finalize(c->F, c->G, c->Z, c->n, n0, mF0, mG0, c->cplx, sort, sF, sG, s, Uo, Vo, Zo, sigF, sigG,
+                       sig, c->d_fin, c->d_status, c->stream);
+  if (rc) return fail(c, rc, "finalize launch");
+  if ((e = cudaMemcpyAsync(c->h_ctr, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "status copy");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "finalize");
+  std::memcpy(&st, c->h_ctr, 4);
+  if (st) return fail(c, HZG_RANK, "bordered solve mixed padded and original columns");
+  return HZG_OK;
+}
+
+int hzg_test_block(int32_t tw, int32_t is_complex, const hzg_config* cfg, double epsn, const double* gFr,
+                   const double* gFi, const double* gGr, const double* gGi, double* zr, double* zi,
+                   int32_t* counts4) {
+  if (!cfg || tw < 2 || tw % 2) return HZG_INVALID;
+  const int NP = is_complex ? 2 : 1;
+  const size_t t2 = (size_t)tw * tw;
+  hzg_ctx c;
+  c.cfg = *cfg;
+  if (c.cfg.max_inner_sweeps <= 0) c.cfg.max_inner_sweeps = 30;
+  c.cplx = is_complex ? 1 : 0;
+  c.tw = tw;
+  c.w = tw / 2;
+  c.epsn = epsn;
+  std::vector<int32_t> inner;
+  int isteps = gen_table(cfg->inner_mm != 0, tw, inner);
+  // device buffers: part (2 mats x NP x t2), zt, ident, counts, itable, colpair
+  double *d_part = nullptr, *d_zt = nullptr;
+  int32_t *d_misc = nullptr;
+  cudaMalloc(&d_part, 2 * NP * t2 * 8);
+  cudaMalloc(&d_zt, NP * t2 * 8);
+  cudaMalloc(&d_misc, (16 + (size_t)isteps * tw) * 4);
+  std::vector<double> hp(2 * NP * t2, 0.0);
+  std::memcpy(hp.data(), gFr, t2 * 8);
+  if (is_complex) std::memcpy(hp.data() + t2, gFi, t2 * 8);
+  std::memcpy(hp.data() + NP * t2, gGr, t2 * 8);
+  if (is_complex) std::memcpy(hp.data() + NP * t2 + t2, gGi, t2 * 8);
+  cudaMemcpy(d_part, hp.data(), hp.size() * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(d_misc + 16, inner.data(), (size_t)isteps * tw * 4, cudaMemcpyHostToDevice);
+  cudaMemset(d_misc, 0, 16 * 4);
+  GramWS gw{};
+  gw.part = d_part;
+  gw.nsplit[0] = gw.nsplit[1] = 1;
+  gw.smax = 1;
+  gw.chunk[0] = gw.chunk[1] = 1;
+  InnerOut io{d_zt, d_misc, d_misc + 4};
+  StepPairs sp{d_misc + 8, 1};  // colpair (0, w): only used by the QR fallback
+  KernelCfg kc = kernel_cfg(&c);
+  kc.fallback_qr = 0;  // the block test has no columns to shorten
+  Plane dummy{nullptr, nullptr, 0, 0};
+  int rc = launch_inner(dummy, dummy, sp, 0, kc, gw, d_misc + 16, isteps, io, nullptr, 1, d_misc + 12, 0);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (rc == HZG_OK && e == cudaSuccess) {
+    std::vector<double> hz(NP * t2);
+    cudaMemcpy(hz.data(), d_zt, NP * t2 * 8, cudaMemcpyDeviceToHost);
+    std::memcpy(zr, hz.data(), t2 * 8);
+    if (is_complex && zi) std::memcpy(zi, hz.data() + t2, t2 * 8);
+    cudaMemcpy(counts4, d_misc + 4, 16, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d_part);
+  cudaFree(d_zt);
+  cudaFree(d_misc);
+  if (rc) return rc;
+  return e == cudaSuccess ? HZG_OK : HZG_CUDA;
+}
+
+const char* hzg_last_error(const hzg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void hzg_destroy(hzg_ctx* c) {
+  if (!c) return;
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->cap) cudaStreamDestroy(c->cap);
+  if (c->h_ctr) cudaFreeHost(c->h_ctr);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// Internal host/device declarations shared by the hzg translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hzg {
+
+// status bits written per block pair (and OR-folded per sweep)
+enum : int {
+  ST_OK = 0,
+  ST_RANK = 1,        // zero column / zero pencil (RankError)
+  ST_NOT_PD = 2,      // Cholesky failed with the QR fallback disabled
+  ST_QR_RANK = 4,     // QR shortening found a rank-deficient block (RankError)
+};
+
+
+// One matrix of the pair in HBM: split planes, column-major, column j at
+// re + j * ld (the reference's Fortran MatrixPlanePair, core.py:26-69).
+struct Plane {
+  double* re;
+  double* im;  // nullptr for real problems
+  int64_t rows;
+  int64_t ld;
+};
+
+// Per-step view of the block pairs this GPU processes.  colpair[k] holds the
+// physical column offsets (c0, c1) of pair k of the step: c0 is the block
+// with the smaller logical index (the reference's sorted (p, q), blocked.py:438-439).
+struct StepPairs {
+  const int32_t* colpair;  // [osteps][npairs][2]
+  int npairs;
+};
+
+struct KernelCfg {
+  int tw;               // 2w
+  int cplx;
+  int prescale;         // pointwise.py:78
+  int per_step_rescale; // !prescale
+  int compensated;
+  int crit_c2;
+  int sorting;
+  int max_inner_sweeps;
+  int fallback_qr;
+  double epsn;          // gate_eps * sqrt(n) (blocked.py:571-572)
+};
+
+// Grammian partials: [pair][mat(F,G)][split][plane][tw*tw], element (r,s) at s*tw+r.
+struct GramWS {
+  double* part;
+  int nsplit[2];   // splits per matrix (powers of two)
+  int smax;        // stride (max of nsplit)
+  int64_t chunk[2];  // rows per split (powers of two in exact mode)
+};
+
+// per-pair outputs of the inner kernel
+struct InnerOut {
+  double* zt;        // [pair][plane][tw*tw]
+  int32_t* ident;    // [pair] 1 -> transform is exactly I (skip postmult, blocked.py:480)
+  int32_t* counts;   // [osteps][npairs][4]: total, big, status, inner sweeps
+};
+
+// kernel launchers (hzg_kernels.cu / hzg_dmma.cu)
+int launch_prescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, int cplx, int do_prescale,
+                    int32_t* status, cudaStream_t s);
+int launch_rescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, int cplx, int final, double* sigF,
+                   double* sigG, double* sig, const int64_t* gate_counters, int32_t* status, cudaStream_t s);
+int launch_gram_exact(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
+                      const GramWS& gw, cudaStream_t s);
+int launch_gram_dmma(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
+                     const GramWS& gw, cudaStream_t s);
+int launch_inner(const Plane& F, const Plane& G, const StepPairs& sp, int step, const KernelCfg& kc,
+                 const GramWS& gw, const int32_t* itable, int isteps, const InnerOut& io, double* qr_scratch,
+                 int qr_slots, int32_t* qr_slot_ctr, cudaStream_t s);
+int launch_postmult_exact(const Plane& F, const Plane& G, const Plane& Z, const StepPairs& sp, int step, int w,
+                          int cplx, const InnerOut& io, cudaStream_t s);
+int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const StepPairs& sp, int step, int w,
+                         int cplx, const InnerOut& io, cudaStream_t s);
+int launch_counters(const int32_t* counts, int64_t nentries, int64_t* out, cudaStream_t s);
+int launch_finalize(const Plane& U, const Plane& V, const Plane& Z, int64_t n, int64_t n0, int64_t mF0, int64_t mG0,
+                    int cplx, int sort, const double* sigF, const double* sigG, const double* sig, Plane Uo, Plane Vo,
+                    Plane Zo, double* sFo, double* sGo, double* so, int32_t* rank_ws, int32_t* status,
+                    cudaStream_t s);
+
+bool dmma_supported(int w);
+
+}  // namespace hzg

@@ -1,0 +1,248 @@
+"""The GSVD entry points on the B200 path.
+
+``solve`` keeps the reference's contract (blocked.py:640-663): numpy or
+MatrixPlanePair inputs, bordering, unbordering and a stable descending sort,
+a GsvdResult of numpy planes.  Underneath, the pair is copied to the GPU,
+bordered there, and every outer sweep runs in libhzg.so (hzg_sweep); only
+the two sweep counters come back to the host per sweep.
+
+``DeviceGsvd`` is the device-resident form used by the benchmark and by
+callers that already hold torch tensors: planes stay in HBM from input to
+output.
+"""
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _native
+from .config import SolverConfig
+from .core import GsvdResult, MatrixPlanePair, ProblemPair, bordered_shape
+from .errors import DeviceError, RankError
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the B200 path has no CPU fallback")
+    return torch
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class DeviceGsvd:
+    """One bordered problem resident on a GPU.
+
+    planes: dict with keys Fr, Fi, Gr, Gi (torch float64 tensors of shape
+    (n, m) -- column-major planes; imaginary ones None for real problems)
+    already bordered to multiples of 2w.  Z planes and the workspace are
+    allocated here.
+    """
+
+    def __init__(self, planes, cfg, device=None, epsn=None, schedule=None):
+        torch = _torch()
+        self.cfg = cfg
+        self.torch = torch
+        Fr, Gr = planes["Fr"], planes["Gr"]
+        self.device = Fr.device if device is None else torch.device(device)
+        self.n, self.mF = Fr.shape
+        self.mG = Gr.shape[1]
+        self.cplx = planes.get("Fi") is not None
+        self.planes = planes
+        lib = _native.load()
+        self.lib = lib
+        ccfg = _native.make_config(cfg)
+        ctx = ctypes.c_void_p()
+        _native.check(lib.hzg_create(ctypes.byref(ctx), self.device.index or 0, self.mF, self.mG, self.n,
+                                     int(self.cplx), ctypes.byref(ccfg), float(epsn or 0.0)),
+                      None, "hzg_create (n=%d, mF=%d, mG=%d, w=%d)" % (self.n, self.mF, self.mG, cfg.block_width))
+        self.ctx = ctx
+        if schedule is not None:
+            sched = np.ascontiguousarray(schedule, dtype=np.int32)
+            _native.check(lib.hzg_set_schedule(ctx, sched.ctypes.data_as(ctypes.c_void_p), sched.shape[0],
+                                               sched.shape[1]), ctx, "hzg_set_schedule")
+        kw = dict(dtype=torch.float64, device=self.device)
+        self.Zr = torch.empty((self.n, self.n), **kw)
+        self.Zi = torch.empty((self.n, self.n), **kw) if self.cplx else None
+        self.ws = torch.empty(int(lib.hzg_workspace_bytes(ctx)), dtype=torch.uint8, device=self.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        _native.check(lib.hzg_bind(ctx, _ptr(Fr), _ptr(planes.get("Fi")), _ptr(Gr), _ptr(planes.get("Gi")),
+                                   _ptr(self.Zr), _ptr(self.Zi), _ptr(self.ws),
+                                   ctypes.c_void_p(self.stream.cuda_stream)), ctx, "hzg_bind")
+        self.sweeps = 0
+        self.total = 0
+        self.big = 0
+        self.converged = False
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            self.lib.hzg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def init(self):
+        _native.check(self.lib.hzg_init_fgz(self.ctx), self.ctx, "prescale")
+
+    def sweep(self):
+        tot = ctypes.c_int64(0)
+        big = ctypes.c_int64(0)
+        _native.check(self.lib.hzg_sweep(self.ctx, ctypes.byref(tot), ctypes.byref(big)), self.ctx, "sweep")
+        return tot.value, big.value
+
+    def run(self, max_sweeps=None):
+        """_algorithm1_loop (blocked.py:503-550) with the device doing the work."""
+        self.init()
+        cap = self.cfg.max_outer_sweeps if max_sweeps is None else max_sweeps
+        for _ in range(cap):
+            t, b = self.sweep()
+            self.sweeps += 1
+            self.total += t
+            self.big += b
+            if b == 0:
+                self.converged = True
+                break
+        return self
+
+    def run_steps(self, first, count):
+        _native.check(self.lib.hzg_run_steps(self.ctx, first, count), self.ctx, "run_steps")
+
+    def finalize(self, n0=None, mF0=None, mG0=None, sort=True):
+        """Final rescale, unborder, sort; returns device output tensors."""
+        torch = self.torch
+        n0 = self.n if n0 is None else n0
+        mF0 = self.mF if mF0 is None else mF0
+        mG0 = self.mG if mG0 is None else mG0
+        kw = dict(dtype=torch.float64, device=self.device)
+        out = dict(Ur=torch.empty((n0, mF0), **kw), Vr=torch.empty((n0, mG0), **kw),
+                   Zr=torch.empty((n0, n0), **kw), sigmaF=torch.empty(n0, **kw), sigmaG=torch.empty(n0, **kw),
+                   sigma=torch.empty(n0, **kw))
+        for k, shape in (("Ui", (n0, mF0)), ("Vi", (n0, mG0)), ("Zi", (n0, n0))):
+            out[k] = torch.empty(shape, **kw) if self.cplx else None
+        _native.check(self.lib.hzg_finalize(self.ctx, n0, mF0, mG0, int(bool(sort)), _ptr(out["Ur"]),
+                                            _ptr(out["Ui"]), _ptr(out["Vr"]), _ptr(out["Vi"]), _ptr(out["Zr"]),
+                                            _ptr(out["Zi"]), _ptr(out["sigmaF"]), _ptr(out["sigmaG"]),
+                                            _ptr(out["sigma"])), self.ctx, "finalize")
+        return out
+
+
+def _planes_of(m):
+    """numpy (re, im or None) Fortran planes of a MatrixPlanePair."""
+    return m.re, (m.im if m.is_complex else None)
+
+
+def upload_bordered(F, G, w, device=None, torch=None):
+    """Copy (F, G) to the GPU and border them there exactly like
+    border_pair(p, 2w, 2w) (core.py:186-218): pad columns carry a single 1
+    on the extended diagonal, pad rows are zero."""
+    torch = torch or _torch()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    n0 = F.cols
+    padF, mF = bordered_shape(n0, F.rows, 2 * w, 2 * w)
+    padG, mG = bordered_shape(n0, G.rows, 2 * w, 2 * w)
+    n = n0 + padF
+    out = {}
+    for key, M, m in (("F", F, mF), ("G", G, mG)):
+        re, im = _planes_of(M)
+        for suffix, host in (("r", re), ("i", im)):
+            if host is None:
+                out[key + suffix] = None
+                continue
+            d = torch.zeros((n, m), dtype=torch.float64, device=dev)
+            h = torch.from_numpy(np.asfortranarray(host).T)
+            d[:n0, :M.rows].copy_(h, non_blocking=True)
+            if suffix == "r" and padF:
+                k = torch.arange(padF, device=dev)
+                d[n0 + k, M.rows + k] = 1.0
+            out[key + suffix] = d
+    return out, n, mF, mG
+
+
+def _to_numpy_plane(t):
+    """(cols, rows) device tensor -> Fortran (rows, cols) numpy plane."""
+    return t.cpu().numpy().T
+
+
+def gsvd_1x1(F, G):
+    """Closed form for a single-column pair (pointwise.py:324-345)."""
+    from .reftree import norm_sq
+    f = F.to_dense()[:, 0]
+    g = G.to_dense()[:, 0]
+    nf2 = norm_sq(f, F.field)
+    ng2 = norm_sq(g, G.field)
+    if not (nf2 > 0.0 and ng2 > 0.0):
+        raise RankError("zero column in a 1x1 problem")
+    nf = math.sqrt(nf2)
+    ng = math.sqrt(ng2)
+    rt = math.sqrt(nf2 + ng2)
+    z = 1.0 / rt
+    U = MatrixPlanePair.from_dense((f * (1.0 / nf)).reshape(-1, 1))
+    V = MatrixPlanePair.from_dense((g * (1.0 / ng)).reshape(-1, 1))
+    Z = MatrixPlanePair.from_dense(np.array([[z]]) if not F.is_complex else np.array([[complex(z, 0.0)]]))
+    return GsvdResult(U, V, Z, np.array([nf / rt]), np.array([ng / rt]), np.array([nf / ng]), sweeps=0,
+                      total_transforms=0, big_transforms=0, converged=True)
+
+
+def _result_from_device(dev, out, cplx, workers=1):
+    def plane(kr, ki):
+        re = _to_numpy_plane(out[kr])
+        im = _to_numpy_plane(out[ki]) if cplx else None
+        return MatrixPlanePair(re.shape[0], re.shape[1], re, im, cplx)
+
+    return GsvdResult(plane("Ur", "Ui"), plane("Vr", "Vi"), plane("Zr", "Zi"), out["sigmaF"].cpu().numpy(),
+                      out["sigmaG"].cpu().numpy(), out["sigma"].cpu().numpy(), sweeps=dev.sweeps,
+                      total_transforms=dev.total, big_transforms=dev.big, converged=dev.converged,
+                      workers=workers)
+
+
+def gsvd_blocked(p, cfg=None, epsn=None):
+    """Full blocked solve of a bordered pair (column count a multiple of 2w),
+    without unbordering or sorting (blocked.py:553-586)."""
+    cfg = cfg or SolverConfig()
+    w = cfg.block_width
+    if p.n % (2 * w) != 0:
+        raise ValueError("blocked solver needs n divisible by 2w; border first")
+    # row counts that are not multiples of 2w are zero-padded on the device
+    # (zero rows change no inner product) and cropped again by finalize
+    planes, n, mF, mG = upload_bordered(p.F, p.G, w)
+    dev = DeviceGsvd(planes, cfg, epsn=epsn)
+    dev.run()
+    out = dev.finalize(n, p.F.rows, p.G.rows, sort=False)
+    r = _result_from_device(dev, out, p.is_complex)
+    dev.close()
+    return r
+
+
+def solve(F, G, cfg=None, workers=1, worker_sweeps=1):
+    """Border, solve on the GPU, unborder, and sort a GSVD problem.
+
+    F and G may be MatrixPlanePair values or numpy arrays.  ``workers``
+    records the number of cooperating GPUs; results do not depend on it
+    (the block schedule is GPU-count invariant, see strategies.py), so a
+    single-process call runs the whole schedule on the current device.
+    """
+    cfg = cfg or SolverConfig()
+    if isinstance(F, np.ndarray):
+        F = MatrixPlanePair.from_dense(F)
+    if isinstance(G, np.ndarray):
+        G = MatrixPlanePair.from_dense(G)
+    if workers < 1:
+        raise ValueError("need at least one worker")
+    if F.cols == 1:
+        return gsvd_1x1(F, G)
+    p = ProblemPair(F, G)
+    planes, n, mF, mG = upload_bordered(p.F, p.G, cfg.block_width)
+    dev = DeviceGsvd(planes, cfg)
+    try:
+        dev.run()
+        out = dev.finalize(p.n, p.F.rows, p.G.rows, sort=True)
+        return _result_from_device(dev, out, p.is_complex, workers)
+    finally:
+        dev.close()

@@ -1,0 +1,215 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle / reference.
+
+* exact mode (reference-order Grammian and postmultiply kernels): bitwise
+  equal to the reference's outputs on every golden case;
+* inner block kernel (Cholesky + pointwise sweeps + theta rescale):
+  bitwise equal to the oracle on random block Grammians;
+* default DMMA mode: within the north-star tolerances (stated per test),
+  bitwise reproducible run to run.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_1909_00101_b200 as hz
+from paper_1909_00101_b200 import _native
+from conftest import gsvd_metrics, load_case, manifest, rel_err_sorted
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+EPS = 2.0 ** -52
+CASES = sorted(manifest())
+
+
+def _cfg(c, **kw):
+    d = dict(c["cfg"])
+    d.update(kw)
+    return hz.SolverConfig(**d)
+
+
+# ---------------------------------------------------------------------------
+# exact mode: bitwise against the reference's own outputs
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", CASES)
+def test_exact_mode_bitwise_vs_reference(name):
+    c = load_case(name)
+    r = hz.solve(c["F"], c["G"], _cfg(c, exact=True))
+    assert [r.sweeps, r.total_transforms, r.big_transforms, int(r.converged)] == list(c["counters"])
+    assert np.array_equal(r.sigma, c["sigma"])
+    assert np.array_equal(r.sigmaF, c["sigmaF"])
+    assert np.array_equal(r.sigmaG, c["sigmaG"])
+    if c["full"]:
+        assert np.array_equal(r.U.to_dense(), c["U"])
+        assert np.array_equal(r.V.to_dense(), c["V"])
+        assert np.array_equal(r.Z.to_dense(), c["Z"])
+
+
+# ---------------------------------------------------------------------------
+# the inner block kernel, bitwise against the oracle
+# ---------------------------------------------------------------------------
+
+def _random_grams(tw, cplx, seed, m=None):
+    rng = np.random.default_rng(seed)
+    m = m or 3 * tw
+    Y = rng.standard_normal((m, tw)) + (1j * rng.standard_normal((m, tw)) if cplx else 0)
+    Gm = rng.standard_normal((m, tw)) + (1j * rng.standard_normal((m, tw)) if cplx else 0)
+    Gm = Gm / np.linalg.norm(Gm, axis=0)
+    out = []
+    for M in (Y, Gm):
+        Ar, Ai = O.grammian(np.asfortranarray(M.real), np.asfortranarray(M.imag) if cplx else None, 0, tw // 2,
+                            tw // 2, cplx)
+        out.append((Ar, Ai))
+    return out
+
+
+def _gpu_block(tw, cplx, cfg, epsn, grams):
+    (Fr, Fi), (Gr, Gi) = grams
+    ccfg = _native.make_config(cfg)
+    zr = np.zeros((tw, tw), order="F")
+    zi = np.zeros((tw, tw), order="F")
+    cnt = np.zeros(4, dtype=np.int32)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    rc = _native.load().hzg_test_block(tw, int(cplx), ctypes.byref(ccfg), epsn, p(Fr), p(Fi), p(Gr), p(Gi),
+                                       p(zr), p(zi), p(cnt))
+    assert rc == 0
+    return (zr + 1j * zi if cplx else zr), cnt
+
+
+@pytest.mark.parametrize("tw", [2, 4, 8, 16, 32, 64])
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("variant", [0, 2, 4, 6])
+def test_inner_block_kernel_bitwise(tw, cplx, variant):
+    cfg = hz.SolverConfig(variant_id=variant, block_width=tw // 2)
+    epsn = EPS * np.sqrt(1024.0)
+    for seed in range(3):
+        grams = _random_grams(tw, cplx, 1000 * tw + seed)
+        (Fr, Fi), (Gr, Gi) = grams
+        Fh, st1 = O.cholesky_upper(Fr + 1j * Fi if cplx else Fr)
+        Gh, st2 = O.cholesky_upper(Gr + 1j * Gi if cplx else Gr)
+        assert st1 == 0 and st2 == 0
+        _, _, Zo, tot, big, st = O.block_inner(Fh, Gh, O.cfg_from(cfg), epsn)
+        assert st == 0
+        Zg, cnt = _gpu_block(tw, cplx, cfg, epsn, grams)
+        assert cnt[2] == 0
+        assert (cnt[0], cnt[1]) == (tot, big)
+        assert np.array_equal(Zg, Zo), "tw=%d cplx=%s variant=%d seed=%d" % (tw, cplx, variant, seed)
+
+
+@pytest.mark.parametrize("kw", [dict(sorting=False), dict(inner_kind="mm"), dict(blocking="bo")])
+def test_inner_block_kernel_bitwise_options(kw):
+    tw = 32
+    cfg = hz.SolverConfig(block_width=16, **kw)
+    epsn = EPS * np.sqrt(4096.0)
+    for cplx in (False, True):
+        grams = _random_grams(tw, cplx, 77)
+        (Fr, Fi), (Gr, Gi) = grams
+        Fh, _ = O.cholesky_upper(Fr + 1j * Fi if cplx else Fr)
+        Gh, _ = O.cholesky_upper(Gr + 1j * Gi if cplx else Gr)
+        _, _, Zo, tot, big, st = O.block_inner(Fh, Gh, O.cfg_from(cfg), epsn)
+        Zg, cnt = _gpu_block(tw, cplx, cfg, epsn, grams)
+        assert (cnt[0], cnt[1], cnt[2]) == (tot, big, 0)
+        assert np.array_equal(Zg, Zo)
+
+
+def test_inner_block_kernel_not_pd_signal():
+    tw = 8
+    A = np.ones((tw, tw))  # rank one: Cholesky fails at the second pivot
+    cfg = hz.SolverConfig(block_width=4, fallback_qr=False)
+    Zg, cnt = _gpu_block(tw, False, cfg, 1e-14, [(np.asfortranarray(A), np.zeros((tw, tw))),
+                                                 (np.asfortranarray(np.eye(tw)), np.zeros((tw, tw)))])
+    assert cnt[2] == 2
+
+
+# ---------------------------------------------------------------------------
+# DMMA mode: tolerance parity + reproducibility
+# ---------------------------------------------------------------------------
+
+DMMA_CASES = [n for n in CASES if manifest()[n]["cfg"].get("block_width", 8) in (8, 16)]
+
+
+@pytest.mark.parametrize("name", DMMA_CASES)
+def test_dmma_mode_within_tolerance(name):
+    c = load_case(name)
+    n = c["n"]
+    r = hz.solve(c["F"], c["G"], _cfg(c))
+    # tolerances: sigma rel err <= 8 n eps vs the reference
+    # (floored at n = 64); residuals <= 4 n eps; orthogonality <= 32 n eps
+    nn = max(n, 64)
+    assert r.converged
+    assert rel_err_sorted(r.sigma, c["sigma"]).max() <= 8 * nn * EPS
+    m = gsvd_metrics(c["F"], c["G"], r)
+    assert m["resF"] <= 4 * nn * EPS and m["resG"] <= 4 * nn * EPS
+    assert m["orthU"] <= 32 * nn * EPS and m["orthV"] <= 32 * nn * EPS
+    assert m["pencil"] <= 1e-14
+    ratio = r.sigmaF / r.sigmaG
+    assert np.all(np.abs(r.sigma - ratio) <= 2 * np.spacing(np.abs(ratio)))
+    assert abs(r.sweeps - c["counters"][0]) <= 2
+
+
+def test_dmma_mode_bitwise_repeatable():
+    c = load_case("genpair256_w16")
+    a = hz.solve(c["F"], c["G"], _cfg(c))
+    b = hz.solve(c["F"], c["G"], _cfg(c))
+    assert np.array_equal(a.sigma, b.sigma)
+    assert np.array_equal(a.U.re, b.U.re) and np.array_equal(a.Z.re, b.Z.re)
+    assert (a.sweeps, a.total_transforms, a.big_transforms) == (b.sweeps, b.total_transforms, b.big_transforms)
+
+
+def test_power_of_two_scaling_invariance():
+    c = load_case("genpair256_w16")
+    a = hz.solve(c["F"], c["G"], _cfg(c))
+    b = hz.solve(c["F"] * 2.0, c["G"] * 2.0, _cfg(c))
+    assert np.array_equal(a.sigma, b.sigma)
+
+
+def test_config2_1024_bitwise_reproducible_and_accurate():
+    g = O.gaussian_stream(1024, 2 * 1024 * 1024)
+    F = g[: 1024 * 1024].reshape((1024, 1024), order="F")
+    G = g[1024 * 1024:].reshape((1024, 1024), order="F")
+    cfg = hz.SolverConfig(block_width=16)
+    runs = [hz.solve(F, G, cfg) for _ in range(3)]
+    for r in runs[1:]:
+        for a, b in ((r.U.re, runs[0].U.re), (r.V.re, runs[0].V.re), (r.Z.re, runs[0].Z.re),
+                     (r.sigma, runs[0].sigma), (r.sigmaF, runs[0].sigmaF), (r.sigmaG, runs[0].sigmaG)):
+            assert np.array_equal(a, b)
+        assert (r.sweeps, r.total_transforms, r.big_transforms) == \
+            (runs[0].sweeps, runs[0].total_transforms, runs[0].big_transforms)
+    m = gsvd_metrics(F, G, runs[0])
+    n = 1024
+    assert m["resF"] <= 4 * n * EPS and m["resG"] <= 4 * n * EPS
+    assert m["orthU"] <= 32 * n * EPS and m["orthV"] <= 32 * n * EPS
+    ref = np.sort(np.linalg.svd(F @ np.linalg.inv(G), compute_uv=False))[::-1]
+    assert rel_err_sorted(runs[0].sigma, ref).max() <= 1e-9
+
+
+def test_exact_vs_oracle_on_bordered_complex():
+    rng = np.random.default_rng(5)
+    F = rng.standard_normal((70, 45)) + 1j * rng.standard_normal((70, 45))
+    G = rng.standard_normal((50, 45)) + 1j * rng.standard_normal((50, 45))
+    cfg = hz.SolverConfig(block_width=8, exact=True)
+    r = hz.solve(F, G, cfg)
+    o = O.solve(F, G, O.cfg_from(cfg))
+    assert np.array_equal(r.sigma, o["sigma"])
+    assert np.array_equal(r.Z.to_dense(), o["Z"])
+    assert r.sigma.size == 45 and r.U.rows == 70 and r.V.rows == 50
+
+
+def test_rank_error_on_zero_column():
+    F = np.eye(16)
+    G = np.eye(16)
+    G[:, 3] = 0.0
+    with pytest.raises(hz.RankError):
+        hz.solve(F, G, hz.SolverConfig(block_width=4))
+
+
+def test_gsvd_blocked_unsorted_and_identity():
+    eye = hz.MatrixPlanePair.from_dense(np.eye(16))
+    r = hz.gsvd_blocked(hz.ProblemPair(eye, eye), hz.SolverConfig(block_width=4))
+    assert r.sweeps == 1 and r.converged
+    np.testing.assert_allclose(r.sigma, 1.0, rtol=4 * EPS)
+    np.testing.assert_allclose(np.diag(r.Z.re), 1 / np.sqrt(2.0), rtol=4 * EPS)
+    np.testing.assert_array_equal(r.U.re, np.eye(16))
