@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 GSVD path (BASELINE.json metric: GSVD wall time and
+FP64 GFLOP/s).
+
+A step is one complete GSVD of the configured synthetic pair: prescale, all
+outer sweeps to convergence, final rescale, unborder and sort.
+
+* value  -- inputs resident in HBM (device-to-device refresh of the working
+            planes is inside the step), outputs left in HBM; FP64 GFLOP/s of
+            the algorithmic count:
+            sweeps * P * c * [12 w^2 (mF + mG) + 8 w^2 n],  P = Nb (Nb - 1) / 2.
+* e2e    -- the same through the public drop-in API solve(): numpy inputs in
+            pinned host memory copied in, numpy U, V, Z, sigma copied out.
+* roofline -- per-kernel CUDA-event times captured inside the sweep graph
+            over the timed region; algorithmic bytes per launch / avg time.
+* cpu_baseline -- the CPU oracle (C restatement, bitwise the reference) on
+            a bounded sample of outer steps, all host threads.
+
+`--impl reference` times the reference CPU path (the oracle port) alone.
+Multi-GPU (torchrun): independent replicas, one problem per rank (weak
+scaling); the time is the max over ranks.
+"""
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GSVD wall time (s) and FP64 GFLOP/s at n=4096/16384, 1/2/4/8 B200 vs CPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--kind", default="cond", choices=["cond", "gauss"],
+                    help="cond: config 4 (sigma in [1e-8, 1e8]); gauss: iid Gaussian (config 5)")
+    ap.add_argument("--w", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=4096)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+
+def workload_name(a):
+    if a.kind == "cond":
+        return ("config4: real FP64 F,G %dx%d, generalized singular values logspace(1e-8,1e8) shuffled, "
+                "F=U diag(sF) X, G=V diag(sG) X (U,V Haar, X=W diag(U[0.01,1]) W^T), w=%d, full GSVD per step"
+                % (a.n, a.n, a.w))
+    return "real FP64 iid-Gaussian F,G %dx%d, w=%d, full GSVD per step" % (a.n, a.n, a.w)
+
+
+def gen_pair(a, torch, device):
+    """Synthetic pair as column-major planes: torch tensors (n, m)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(a.seed)
+    n = a.n
+    kw = dict(dtype=torch.float64, device=device)
+    if a.kind == "gauss":
+        F = torch.randn((n, n), generator=g, **kw)
+        G = torch.randn((n, n), generator=g, **kw)
+        return F.T.contiguous(), G.T.contiguous(), None
+
+    def haar():
+        q, r = torch.linalg.qr(torch.randn((n, n), generator=g, **kw))
+        return q * torch.sign(torch.diagonal(r))[None, :]
+
+    sig = torch.logspace(-8, 8, n, **kw)[torch.randperm(n, generator=g, device=device)]
+    sF = sig / torch.sqrt(1 + sig * sig)
+    sG = 1 / torch.sqrt(1 + sig * sig)
+    U, V, W = haar(), haar(), haar()
+    lam = 0.01 + 0.99 * torch.rand(n, generator=g, **kw)
+    X = (W * lam[None, :]) @ W.T
+    F = U @ (sF[:, None] * X)
+    G = V @ (sG[:, None] * X)
+    return F.T.contiguous(), G.T.contiguous(), sig
+
+
+def flops_per_sweep(n, mF, mG, w, cplx=False):
+    nb = n // w
+    P = nb * (nb - 1) // 2
+    c = 4 if cplx else 1
+    return P * c * (12 * w * w * (mF + mG) + 8 * w * w * n)
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (the oracle -- C restatement of the reference, bitwise pinned)
+# ---------------------------------------------------------------------------
+
+def cpu_sample(Fp, Gp, w, cfg_kw, budget_s, threads):
+    """Time outer steps of sweep 1 of the oracle on the bordered planes.
+    Returns (steps, seconds, flops)."""
+    import numpy as np
+    from oracle import oracle as O
+    n, mF = Fp.shape[1], Fp.shape[0]
+    mG = Gp.shape[0]
+    cfg = O.make_cfg(block_width=w, **cfg_kw)
+    osteps = n // w - 1
+    per_step = flops_per_sweep(n, mF, mG, w) / osteps
+    t0 = time.perf_counter()
+    O.gsvd_blocked(Fp, None, Gp, None, False, cfg, threads=threads, step_limit=1)
+    t1 = time.perf_counter() - t0
+    steps = int(max(1, min(osteps, budget_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    O.gsvd_blocked(Fp, None, Gp, None, False, cfg, threads=threads, step_limit=steps)
+    dt = time.perf_counter() - t0
+    return steps, dt, steps * per_step
+
+
+def run_reference(a):
+    """--impl reference: the reference CPU path (oracle port) on host cores."""
+    import numpy as np
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    Fr, Gr, _ = gen_pair(a, torch, "cpu")
+    Fp = np.asfortranarray(Fr.numpy().T)
+    Gp = np.asfortranarray(Gr.numpy().T)
+    threads = os.cpu_count() or 1
+    per = max(1.0, a.cpu_seconds / max(1, a.steps + a.warmup))
+    for _ in range(a.warmup):
+        cpu_sample(Fp, Gp, a.w, {}, per, threads)
+    tot_t, tot_f, tot_s = 0.0, 0.0, 0
+    for _ in range(a.steps):
+        s, dt, fl = cpu_sample(Fp, Gp, a.w, {}, per, threads)
+        tot_t += dt
+        tot_f += fl
+        tot_s += s
+    v = tot_f / tot_t / 1e9
+    n = a.n
+    osteps = n // a.w - 1
+    line = {"metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * tot_t / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": workload_name(a), "n": n, "block_width": a.w,
+                       "sample": "%d outer steps of sweep 1 in total (of %d per sweep)" % (tot_s, osteps)},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                             "sample": "%d outer steps of sweep 1, %d threads" % (tot_s, threads)},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "est_full_sweep_s": tot_t / tot_s * osteps}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 path
+# ---------------------------------------------------------------------------
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1909_00101_b200 as hz
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    a.seed += rank  # independent replica per rank
+
+    Fr0, Gr0, truth = gen_pair(a, torch, device)
+    n = a.n
+    cfg = hz.SolverConfig(block_width=a.w)
+    w = a.w
+    padn = (-n) % (2 * w)
+    assert padn == 0, "bench uses n divisible by 2w"
+    mF = mG = n
+    Fw = torch.empty_like(Fr0)
+    Gw = torch.empty_like(Gr0)
+    dev = hz.DeviceGsvd({"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}, cfg)
+    dev.set_timing(True)
+    F_sweep = flops_per_sweep(n, mF, mG, w)
+
+    def step():
+        Fw.copy_(Fr0)
+        Gw.copy_(Gr0)
+        dev.run()
+        out = dev.finalize(n, mF, mG)
+        return out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        out = step()
+    torch.cuda.synchronize()
+    dev.kernel_times(reset=True)
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sweeps = []
+    for _ in range(a.steps):
+        out = step()
+        sweeps.append(dev.sweeps)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    flops = sum(s * F_sweep for s in sweeps)
+    fl_t = torch.tensor([float(flops)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(fl_t)
+    value = float(fl_t.item()) / (ms_max / 1e3) / 1e9
+    kt = dev.kernel_times(reset=True)
+
+    # accuracy of the last solve (self-consistency + truth), cheap on the GPU
+    acc = {}
+    if rank == 0:
+        Ur, Vr, Zr = out["Ur"], out["Vr"], out["Zr"]
+        sF, sG, s = out["sigmaF"], out["sigmaG"], out["sigma"]
+        Fm, Gm = Fr0.T, Gr0.T
+        Zm = Zr.T
+        acc["resF"] = float(torch.linalg.norm(Fm @ Zm - Ur.T * sF[None, :]) / torch.linalg.norm(Fm))
+        acc["resG"] = float(torch.linalg.norm(Gm @ Zm - Vr.T * sG[None, :]) / torch.linalg.norm(Gm))
+        eye = torch.eye(n, dtype=torch.float64, device=device)
+        acc["orthU"] = float(torch.linalg.norm(Ur @ Ur.T - eye))
+        acc["orthV"] = float(torch.linalg.norm(Vr @ Vr.T - eye))
+        if truth is not None:
+            tr = torch.sort(truth, descending=True).values
+            acc["max_rel_sigma_vs_generator"] = float(torch.max(torch.abs(s - tr) / tr))
+
+    # e2e through the public API with pinned host buffers
+    ke = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 3))
+    Fh = torch.empty(Fr0.shape, dtype=torch.float64, pin_memory=True)
+    Gh = torch.empty(Gr0.shape, dtype=torch.float64, pin_memory=True)
+    Fh.copy_(Fr0)
+    Gh.copy_(Gr0)
+    Fnp = Fh.numpy().T  # Fortran-order (m, n) views of pinned memory
+    Gnp = Gh.numpy().T
+    r = hz.solve(Fnp, Gnp, cfg)  # warm
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_sweeps = []
+    for _ in range(ke):
+        r = hz.solve(Fnp, Gnp, cfg)
+        e2e_sweeps.append(r.sweeps)
+    torch.cuda.synchronize()
+    barrier()
+    te = time.perf_counter() - t0
+    tt = torch.tensor([te], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    te = float(tt.item())
+    fe = torch.tensor([float(sum(s * F_sweep for s in e2e_sweeps))], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(fe)
+    e2e_value = float(fe.item()) / te / 1e9
+    h2d = (mF + mG) * n * 8
+    d2h = (mF + mG + n) * n * 8 + 3 * n * 8
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the streaming kernels (algorithmic bytes per launch)
+    npairs = n // w // 2
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    post_bytes = npairs * 2 * w * 8 * 2 * (mF + mG + n)
+    gram_bytes = npairs * 2 * w * 8 * (mF + mG)
+    post_ms = kt["postmult"][0] / max(1, kt["postmult"][1])
+    gram_ms = kt["grammian"][0] / max(1, kt["grammian"][1])
+    inner_ms = kt["inner"][0] / max(1, kt["inner"][1])
+    tot_k = sum(v[0] for v in kt.values())
+    shares = {k: v[0] / tot_k for k, v in kt.items()} if tot_k > 0 else {}
+    post_gbs = post_bytes / (post_ms / 1e3) / 1e9 if post_ms > 0 else None
+    gram_gbs = gram_bytes / (gram_ms / 1e3) / 1e9 if gram_ms > 0 else None
+    roofline = {"kernel": "k_post_dmma (postmultiply of F, G, Z block pairs)", "bound": "hbm",
+                "achieved": post_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": post_gbs / hbm_peak if post_gbs else None, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
+                "bytes_per_launch": post_bytes, "avg_launch_ms": post_ms,
+                "grammian": {"achieved": gram_gbs, "frac": gram_gbs / hbm_peak if gram_gbs else None,
+                             "bytes_per_launch": gram_bytes, "avg_launch_ms": gram_ms},
+                "inner_avg_launch_ms": inner_ms, "kernel_time_shares": shares,
+                "fp64": {"achieved_tflops": value / 1e3 / world, "peak_tflops": 37.04,
+                         "peak_source": "profiles/r01_fp64_peak.txt (DMMA microbenchmark on this pool's B200)",
+                         "frac": value / 1e3 / world / 37.04}}
+    traffic_file = os.path.join(ROOT, "profiles", "traffic_w%d_n%d.json" % (w, n))
+    if os.path.exists(traffic_file):
+        with open(traffic_file) as fh:
+            roofline["traffic"] = json.load(fh).get("postmult_dram_bytes_per_launch")
+
+    cpu = None
+    if not a.no_cpu and world == 1:
+        Fp = np.asfortranarray(Fr0.cpu().numpy().T)
+        Gp = np.asfortranarray(Gr0.cpu().numpy().T)
+        threads = os.cpu_count() or 1
+        s_cpu, dt, fl = cpu_sample(Fp, Gp, w, {}, a.cpu_seconds, threads)
+        cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+               "sample": "%d of %d outer steps of sweep 1 (oracle = C restatement, bitwise the reference)"
+                         % (s_cpu, n // w - 1),
+               "est_full_solve_s": dt / s_cpu * (n // w - 1) * (sum(sweeps) / len(sweeps))}
+
+    launches_per_solve = [1 + s * (3 * (n // w - 1) + 2) + 1 + 4 for s in sweeps]
+    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated on the GPU)",
+            "config": {"workload": workload_name(a), "n": n, "block_width": w, "sweeps": sweeps,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (F+G+Z = %.0f MB > 126 MB)" % (3 * n * n * 8 / 1e6),
+                       "wall_s_per_solve": ms_max / a.steps / 1e3},
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "steps": ke, "wall_s_per_solve": te / ke},
+            "gpu_launches": int(sum(launches_per_solve)), "clocks": clk, "accuracy": acc}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

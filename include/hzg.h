@@ -100,6 +100,24 @@ int hzg_test_block(int32_t tw, int32_t is_complex, const hzg_config* cfg, double
                    const double* gFi, const double* gGr, const double* gGi, double* zr, double* zi,
                    int32_t* counts4);
 
+/* Per-kernel timing: with on != 0 the captured sweep graph records CUDA
+ * events around every Grammian / inner / postmultiply launch (on the stream
+ * they run on); hzg_kernel_times returns the accumulated milliseconds and
+ * launch counts per kind {grammian, inner, postmultiply} since the last
+ * reset.  Must be set before the first hzg_sweep. */
+int hzg_set_timing(hzg_ctx* ctx, int32_t on);
+int hzg_kernel_times(hzg_ctx* ctx, double* ms3, int64_t* launches3, int32_t reset);
+
+/* Diagnostics: copy the per-step, per-pair counters of the last sweep,
+ * int32 [osteps][npairs][4] = {total, big, status, inner sweeps}, to host
+ * memory.  Returns the number of int32 written via *count. */
+int hzg_step_counters(hzg_ctx* ctx, int32_t* out, int64_t capacity, int64_t* count);
+
+/* Diagnostics: enable (before the first sweep) and read the cycle counts
+ * CTA 0 / warp 0 of the inner kernel spends in its phases A (dot
+ * products), B (2x2 transforms), C (column updates), plus the step count. */
+int hzg_debug_phases(hzg_ctx* ctx, int32_t enable, int64_t* out4);
+
 const char* hzg_last_error(const hzg_ctx* ctx);
 void hzg_destroy(hzg_ctx* ctx);
 

@@ -24,7 +24,8 @@ class HzgConfig(ctypes.Structure):
 
 
 EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_init_fgz", "hzg_sweep",
-           "hzg_run_steps", "hzg_finalize", "hzg_test_block", "hzg_last_error", "hzg_destroy")
+           "hzg_run_steps", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
+           "hzg_step_counters", "hzg_debug_phases", "hzg_last_error", "hzg_destroy")
 
 _lib = None
 _lock = threading.Lock()
@@ -55,10 +56,18 @@ def load(path=LIB_PATH):
         L.hzg_sweep.restype = ctypes.c_int
         L.hzg_run_steps.argtypes = [P, I32, I32]
         L.hzg_run_steps.restype = ctypes.c_int
-        L.hzg_finalize.argtypes = [P, I64, I64, I64] + [P] * 9
+        L.hzg_finalize.argtypes = [P, I64, I64, I64, I32] + [P] * 9
         L.hzg_finalize.restype = ctypes.c_int
         L.hzg_test_block.argtypes = [I32, I32, ctypes.POINTER(HzgConfig), D] + [P] * 6 + [P]
         L.hzg_test_block.restype = ctypes.c_int
+        L.hzg_set_timing.argtypes = [P, I32]
+        L.hzg_set_timing.restype = ctypes.c_int
+        L.hzg_kernel_times.argtypes = [P, P, P, I32]
+        L.hzg_kernel_times.restype = ctypes.c_int
+        L.hzg_step_counters.argtypes = [P, P, I64, ctypes.POINTER(I64)]
+        L.hzg_step_counters.restype = ctypes.c_int
+        L.hzg_debug_phases.argtypes = [P, I32, P]
+        L.hzg_debug_phases.restype = ctypes.c_int
         L.hzg_last_error.argtypes = [P]
         L.hzg_last_error.restype = ctypes.c_char_p
         L.hzg_destroy.argtypes = [P]

@@ -48,8 +48,14 @@ struct hzg_ctx {
   int32_t* d_fin = nullptr;    // 2n int32
   double* d_sig = nullptr;     // 3n
   int64_t* h_ctr = nullptr;    // pinned
+  long long* d_phase = nullptr;
   std::string err;
   bool bound = false;
+  // optional per-kernel timing (events captured into the sweep graph)
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;  // [osteps][4]
+  double kms[3] = {0, 0, 0};
+  int64_t kcnt[3] = {0, 0, 0};
 };
 
 namespace {
@@ -142,7 +148,7 @@ void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
 }
 
 struct Layout {
-  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, total;
+  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, phase, total;
 };
 
 Layout layout(const hzg_ctx* c) {
@@ -167,6 +173,7 @@ Layout layout(const hzg_ctx* c) {
   L.qrlock = take((size_t)c->qr_slots * 4);
   L.fin = take((size_t)2 * c->n * 4);
   L.sig = take((size_t)3 * c->n * 8);
+  L.phase = take(4 * 8);
   L.total = off;
   return L;
 }
@@ -187,17 +194,39 @@ KernelCfg kernel_cfg(const hzg_ctx* c) {
   return k;
 }
 
-int launch_step(hzg_ctx* c, int step, cudaStream_t s) {
+int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr) {
   StepPairs sp{c->d_colpair, c->npairs};
   KernelCfg kc = kernel_cfg(c);
+  if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
   int rc = c->use_dmma ? launch_gram_dmma(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s)
                        : launch_gram_exact(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s);
   if (rc) return rc;
+  if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
   rc = launch_inner(c->F, c->G, sp, step, kc, c->gw, c->d_itable, c->isteps, c->io, c->d_qr, c->qr_slots,
                     c->d_qrlock, s);
   if (rc) return rc;
-  return c->use_dmma ? launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s)
-                     : launch_postmult_exact(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s);
+  if (ev) cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal);
+  rc = c->use_dmma ? launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s)
+                   : launch_postmult_exact(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s);
+  if (rc) return rc;
+  if (ev) cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal);
+  return HZG_OK;
+}
+
+void accumulate_times(hzg_ctx* c) {
+  if (!c->timing || c->tev.empty()) return;
+  for (int st = 0; st < c->osteps; ++st) {
+    cudaEvent_t* e = &c->tev[(size_t)st * 4];
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, e[k], e[k + 1]) == cudaSuccess) {
+        c->kms[k] += ms;
+        c->kcnt[k] += 1;
+      } else {
+        (void)cudaGetLastError();  // do not leave a stale error for the next launch check
+      }
+    }
+  }
 }
 
 int status_code(int64_t st) {
@@ -290,6 +319,8 @@ int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double*
   c->d_qrlock = (int32_t*)(c->ws + L.qrlock);
   c->d_fin = (int32_t*)(c->ws + L.fin);
   c->d_sig = (double*)(c->ws + L.sig);
+  c->d_phase = (long long*)(c->ws + L.phase);
+  c->io.phase = nullptr;
   if ((e = cudaMemcpyAsync(c->d_colpair, c->colpair_host.data(), c->colpair_host.size() * 4,
                            cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
     return cuda_fail(c, e, "upload schedule");
@@ -342,7 +373,12 @@ static int build_graph(hzg_ctx* c) {
   if ((e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
     return cuda_fail(c, e, "begin capture");
   int rc = HZG_OK;
-  for (int st = 0; st < c->osteps && rc == HZG_OK; ++st) rc = launch_step(c, st, c->cap);
+  if (c->timing && c->tev.empty()) {
+    c->tev.resize((size_t)c->osteps * 4);
+    for (auto& e : c->tev) cudaEventCreate(&e);
+  }
+  for (int st = 0; st < c->osteps && rc == HZG_OK; ++st)
+    rc = launch_step(c, st, c->cap, c->timing ? &c->tev[(size_t)st * 4] : nullptr);
   if (rc == HZG_OK) rc = launch_counters(c->io.counts, (int64_t)c->osteps * c->npairs, c->d_ctr, c->cap);
   if (rc == HZG_OK)
     rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 0, nullptr, nullptr, nullptr, c->d_ctr, c->d_status,
@@ -372,6 +408,7 @@ int hzg_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
   if ((e = cudaMemcpyAsync(c->h_ctr + 3, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
     return cuda_fail(c, e, "status copy");
   if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "sweep");
+  accumulate_times(c);
   if (total) *total = c->h_ctr[0];
   if (big) *big = c->h_ctr[1];
   int rc = status_code(c->h_ctr[2]);
@@ -456,7 +493,7 @@ int hzg_test_block(int32_t tw, int32_t is_complex, const hzg_config* cfg, double
   gw.nsplit[0] = gw.nsplit[1] = 1;
   gw.smax = 1;
   gw.chunk[0] = gw.chunk[1] = 1;
-  InnerOut io{d_zt, d_misc, d_misc + 4};
+  InnerOut io{d_zt, d_misc, d_misc + 4, nullptr};
   StepPairs sp{d_misc + 8, 1};  // colpair (0, w): only used by the QR fallback
   KernelCfg kc = kernel_cfg(&c);
   kc.fallback_qr = 0;  // the block test has no columns to shorten
@@ -477,6 +514,50 @@ int hzg_test_block(int32_t tw, int32_t is_complex, const hzg_config* cfg, double
   return e == cudaSuccess ? HZG_OK : HZG_CUDA;
 }
 
+int hzg_set_timing(hzg_ctx* c, int32_t on) {
+  if (!c) return HZG_INVALID;
+  if (c->gexec) return fail(c, HZG_INVALID, "hzg_set_timing must precede the first sweep");
+  c->timing = on != 0;
+  return HZG_OK;
+}
+
+int hzg_kernel_times(hzg_ctx* c, double* ms3, int64_t* launches3, int32_t reset) {
+  if (!c) return HZG_INVALID;
+  for (int k = 0; k < 3; ++k) {
+    if (ms3) ms3[k] = c->kms[k];
+    if (launches3) launches3[k] = c->kcnt[k];
+    if (reset) {
+      c->kms[k] = 0;
+      c->kcnt[k] = 0;
+    }
+  }
+  return HZG_OK;
+}
+
+int hzg_step_counters(hzg_ctx* c, int32_t* out, int64_t capacity, int64_t* count) {
+  if (!c || !c->bound) return HZG_INVALID;
+  const int64_t nn = (int64_t)c->osteps * c->npairs * 4;
+  if (count) *count = nn;
+  if (!out || capacity < nn) return HZG_INVALID;
+  cudaError_t e = cudaMemcpyAsync(out, c->io.counts, nn * 4, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return e == cudaSuccess ? HZG_OK : cuda_fail(c, e, "counter copy");
+}
+
+int hzg_debug_phases(hzg_ctx* c, int32_t enable, int64_t* out4) {
+  if (!c || !c->bound) return HZG_INVALID;
+  if (enable) {
+    if (c->gexec) return fail(c, HZG_INVALID, "enable phase diagnostics before the first sweep");
+    cudaMemsetAsync(c->d_phase, 0, 32, c->stream);
+    c->io.phase = c->d_phase;
+  }
+  if (out4) {
+    cudaMemcpyAsync(out4, c->d_phase, 32, cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+  }
+  return HZG_OK;
+}
+
 const char* hzg_last_error(const hzg_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 void hzg_destroy(hzg_ctx* c) {
@@ -485,6 +566,7 @@ void hzg_destroy(hzg_ctx* c) {
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
+  for (auto& e : c->tev) cudaEventDestroy(e);
   delete c;
 }
 

@@ -200,7 +200,7 @@ struct PostCfg {
   static constexpr int WN = NT_N > 4 ? NT_N / 4 : 1;  // warps along N
   static constexpr int TN = NT_N / WN;                // tiles per warp along N
   static constexpr int NWARP = 4 * WN;
-  static constexpr int NS = (CPLX || TW > 32) ? 2 : 4;
+  static constexpr int NS = (CPLX || TW > 32) ? 2 : 3;
   static constexpr int ZS = TW + 4;  // padded stride of Z~ (column-major)
   static constexpr size_t STAGE = (size_t)NP * TW * kRS;
   static constexpr size_t SMEM = (NS * STAGE + (size_t)NP * TW * ZS) * sizeof(double) + 64;
@@ -320,12 +320,15 @@ __global__ void __launch_bounds__(PostCfg<TW, CPLX>::NWARP * 32) k_post_dmma(Pos
         bulk_s2g(base + pair_col(cp, w, c) * Y.ld + r0, st + (size_t)q * kRS, bytes);
       }
       bulk_commit();
-      if (it + C::NS < ntiles) {
-        bulk_wait_read<0>();
+      // refill the stage drained one iteration ago: its bulk store has had a
+      // whole tile of compute to finish reading shared memory
+      if (it >= 1 && it - 1 + C::NS < ntiles) {
+        bulk_wait_read<1>();
         __syncwarp();
-        int64_t r1 = rbeg + (int64_t)(it + C::NS) * kR;
+        const int sp = (it - 1) % C::NS;
+        int64_t r1 = rbeg + (int64_t)(it - 1 + C::NS) * kR;
         int nv1 = (int)(rend - r1 < kR ? rend - r1 : kR);
-        issue_tile_load<TW, NP>(Y, cp, r1, nv1, st, &full[s], lane);
+        issue_tile_load<TW, NP>(Y, cp, r1, nv1, stages + sp * C::STAGE, &full[sp], lane);
       }
     }
   }

@@ -29,10 +29,11 @@ struct InnerSmem {
   double B[NP][TW * TW];  // G-hat
   double Z[NP][TW * TW];  // Z-hat
   uint8_t tab[TW * TW];   // inner table, (steps, TW/2, 2)
-  int wcnt[TW / 2][2];
+  double pd[TW / 2][9];   // phase A -> B: a11 a22 a12r b11 b22 b12r a12i b12i (stride 9: no bank conflicts)
+  double px[TW / 2][7];   // phase B -> C: z11 z12r z12i z21r z21i z22 (stride 7)
+  int pflag[TW / 2];
+  int stepbad, sw_applied, sw_big;
   int chol_fail[2];
-  int sweeps, total, big;
-  int stop;
 };
 
 // Values of one column held by a warp: lane l owns rows l*EPL .. l*EPL+EPL-1.
@@ -319,7 +320,6 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
   for (int e = tid; e < P.isteps * TW; e += nt) S.tab[e] = (uint8_t)P.itable[e];
   if (tid == 0) {
     S.chol_fail[0] = S.chol_fail[1] = 0;
-    S.stop = 0;
   }
 
   // ---- fold the Grammian partials (pairwise over splits) -----------------
@@ -447,73 +447,150 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
   if (__syncthreads_or(pbad) && status == ST_OK) status = ST_RANK;
 
   // ---- pointwise sweeps (pointwise.py:222-251) ---------------------------
+  // Three phases per inner step, so the scalar 2x2 math runs once per pivot
+  // instead of once per lane of 32:
+  //   A) warp p forms pivot p's six (eight, complex) column dot products by
+  //      a butterfly tree and parks them in shared memory;
+  //   B) warp 0, lane p, runs _k_process_pivot's scalar logic for pivot p
+  //      (gate, transform, big/sort decisions) and parks Z-hat entries;
+  //   C) warp p applies the 2x2 transform / swap to its columns.
   int total = 0, big = 0, sweeps = 0;
   if (status == ST_OK) {
+    const bool prof = P.io.phase != nullptr && blockIdx.x == 0 && tid == 0;
+    long long tA = 0, tB = 0, tC = 0, nstep = 0, c0 = 0, c1 = 0;
     for (int sw = 0; sw < kc.max_inner_sweeps; ++sw) {
-      int wapplied = 0, wbig = 0;
+      int lane_applied = 0, lane_big = 0;  // warp 0, lane p: pivot p's counts this sweep
       for (int st = 0; st < P.isteps; ++st) {
+        if (prof) c0 = clock64();
         const int i = S.tab[(st * NW + warp) * 2];
         const int j = S.tab[(st * NW + warp) * 2 + 1];
+        // ---- phase A
         double fi[EPL], fii[EPL], fj[EPL], fji[EPL], gi[EPL], gii[EPL], gj[EPL], gji[EPL];
         load_col<TW, CPLX>(Ar, Ai, i, lane, fi, fii);
         load_col<TW, CPLX>(Ar, Ai, j, lane, fj, fji);
         load_col<TW, CPLX>(Br, Bi, i, lane, gi, gii);
         load_col<TW, CPLX>(Br, Bi, j, lane, gj, gji);
-        double p[8][EPL];
+        {
+          double p[8][EPL];
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-          p[0][e] = nrm_term<CPLX>(fi[e], fii[e]);
-          p[1][e] = nrm_term<CPLX>(fj[e], fji[e]);
-          p[3][e] = nrm_term<CPLX>(gi[e], gii[e]);
-          p[4][e] = nrm_term<CPLX>(gj[e], gji[e]);
-          if (CPLX) {
-            p[2][e] = dot_re_term(fi[e], fii[e], fj[e], fji[e]);
-            p[6][e] = dot_im_term(fi[e], fii[e], fj[e], fji[e]);
-            p[5][e] = dot_re_term(gi[e], gii[e], gj[e], gji[e]);
-            p[7][e] = dot_im_term(gi[e], gii[e], gj[e], gji[e]);
-          } else {
-            p[2][e] = fi[e] * fj[e];
-            p[5][e] = gi[e] * gj[e];
-            p[6][e] = 0.0;
-            p[7][e] = 0.0;
+          for (int e = 0; e < EPL; ++e) {
+            p[0][e] = nrm_term<CPLX>(fi[e], fii[e]);
+            p[1][e] = nrm_term<CPLX>(fj[e], fji[e]);
+            p[3][e] = nrm_term<CPLX>(gi[e], gii[e]);
+            p[4][e] = nrm_term<CPLX>(gj[e], gji[e]);
+            if (CPLX) {
+              p[2][e] = dot_re_term(fi[e], fii[e], fj[e], fji[e]);
+              p[6][e] = dot_im_term(fi[e], fii[e], fj[e], fji[e]);
+              p[5][e] = dot_re_term(gi[e], gii[e], gj[e], gji[e]);
+              p[7][e] = dot_im_term(gi[e], gii[e], gj[e], gji[e]);
+            } else {
+              p[2][e] = fi[e] * fj[e];
+              p[5][e] = gi[e] * gj[e];
+              p[6][e] = 0.0;
+              p[7][e] = 0.0;
+            }
+          }
+          // Recursive-halving butterfly over the 8 quantities: at xor
+          // distance 1, 2, 4 each lane keeps half of the partial sums and
+          // ships the other half, then xor 8, 16 finish one value per lane.
+          // Every partial is still the sum of two aligned neighbour blocks,
+          // so each total is bitwise the reference's pairwise tree.
+          double v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = EPL == 2 ? p[q][0] + p[q][EPL - 1] : p[q][0];
+          const bool b0 = lane & 1, b1 = (lane >> 1) & 1, b2 = (lane >> 2) & 1;
+          double s4[4], s2[2];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double keep = b0 ? v[q + 4] : v[q], send = b0 ? v[q] : v[q + 4];
+            s4[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const double keep = b1 ? s4[q + 2] : s4[q], send = b1 ? s4[q] : s4[q + 2];
+            s2[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+          }
+          double s1 = (b2 ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? s2[0] : s2[1], 4);
+          s1 = s1 + __shfl_xor_sync(0xffffffffu, s1, 8);
+          s1 = s1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+          if (lane < 8) S.pd[warp][4 * b0 + 2 * b1 + b2] = s1;
+        }
+        __syncthreads();
+        if (prof) {
+          c1 = clock64();
+          tA += c1 - c0;
+          c0 = c1;
+        }
+        // ---- phase B: _k_process_pivot's scalar part (pointwise.py:165-207)
+        if (warp == 0) {
+          int flags = 0;  // 1 applied, 2 big, 4 swap, 8 bad
+          if (lane < NW) {
+            double a11 = S.pd[lane][0], a22 = S.pd[lane][1], a12r = S.pd[lane][2], b11 = S.pd[lane][3];
+            double b22 = S.pd[lane][4], b12r = S.pd[lane][5];
+            double a12i = CPLX ? S.pd[lane][6] : 0.0, b12i = CPLX ? S.pd[lane][7] : 0.0;
+            if (!(a11 > 0.0 && a22 > 0.0 && b11 > 0.0 && b22 > 0.0)) {
+              flags = 8;
+            } else {
+              double d11 = 1.0, d22 = 1.0;
+              if (kc.per_step_rescale) rescale2(a11, a12r, a12i, a22, b11, b12r, b12i, b22, d11, d22);
+              if (gate(a11, a12r, a12i, a22, b12r, b12i, kc.epsn)) {
+                if (kc.sorting && a11 < a22) flags = 4;
+              } else {
+                Xform X = CPLX ? transform_cplx(a11, a12r, a12i, a22, b12r, b12i)
+                               : transform_real(a11, a12r, a22, b12r);
+                int bg = kc.crit_c2 ? !(X.cphi == 1.0 && X.cpsi == 1.0) : !(X.z11 == 1.0 && X.z22 == 1.0);
+                flags = 1 | (bg ? 2 : 0);
+                if (kc.sorting && !CPLX) {
+                  double a1pp, a2pp;
+                  diag_after_real(X.z11, X.z12r, X.z21r, X.z22, a11, a12r, a22, a1pp, a2pp);
+                  if (a1pp < a2pp) flags |= 4;
+                }
+                S.px[lane][0] = X.z11 * d11;
+                S.px[lane][1] = X.z12r * d11;
+                S.px[lane][2] = X.z12i * d11;
+                S.px[lane][3] = X.z21r * d22;
+                S.px[lane][4] = X.z21i * d22;
+                S.px[lane][5] = X.z22 * d22;
+                lane_applied += 1;
+                lane_big += bg;
+              }
+            }
+            S.pflag[lane] = flags;
+          }
+          int anybad = __any_sync(0xffffffffu, flags & 8);
+          if (lane == 0) S.stepbad = anybad;
+          if (st == P.isteps - 1) {
+            int sa = lane_applied, sb = lane_big;
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) {
+              sa += __shfl_xor_sync(0xffffffffu, sa, d);
+              sb += __shfl_xor_sync(0xffffffffu, sb, d);
+            }
+            if (lane == 0) {
+              S.sw_applied = sa;
+              S.sw_big = sb;
+            }
           }
         }
-        constexpr int NV = CPLX ? 8 : 6;
-        double v[8];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) v[q] = EPL == 2 ? p[q][0] + p[q][EPL - 1] : p[q][0];
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-#pragma unroll
-          for (int q = 0; q < NV; ++q) v[q] = v[q] + __shfl_xor_sync(0xffffffffu, v[q], d);
+        __syncthreads();
+        if (prof) {
+          c1 = clock64();
+          tB += c1 - c0;
+          c0 = c1;
         }
-        double a11 = v[0], a22 = v[1], a12r = v[2], b11 = v[3], b22 = v[4], b12r = v[5];
-        double a12i = CPLX ? v[6] : 0.0, b12i = CPLX ? v[7] : 0.0;
-        // _k_process_pivot (pointwise.py:161-219)
-        bool swap = false, wrote = false;
-        int mybad = 0;
-        double zi_[EPL], zii[EPL], zj_[EPL], zji[EPL];
-        if (!(a11 > 0.0 && a22 > 0.0 && b11 > 0.0 && b22 > 0.0)) {
-          mybad = 1;
-        } else {
-          double d11 = 1.0, d22 = 1.0;
-          if (kc.per_step_rescale) rescale2(a11, a12r, a12i, a22, b11, b12r, b12i, b22, d11, d22);
-          if (gate(a11, a12r, a12i, a22, b12r, b12i, kc.epsn)) {
-            swap = kc.sorting && a11 < a22;
-            if (swap) load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii), load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
-          } else {
-            Xform X = CPLX ? transform_cplx(a11, a12r, a12i, a22, b12r, b12i) : transform_real(a11, a12r, a22, b12r);
-            int bg = kc.crit_c2 ? !(X.cphi == 1.0 && X.cpsi == 1.0) : !(X.z11 == 1.0 && X.z22 == 1.0);
-            if (kc.sorting && !CPLX) {
-              double a1pp, a2pp;
-              diag_after_real(X.z11, X.z12r, X.z21r, X.z22, a11, a12r, a22, a1pp, a2pp);
-              swap = a1pp < a2pp;
-            }
-            double z11 = X.z11 * d11, z12r = X.z12r * d11, z12i = X.z12i * d11;
-            double z21r = X.z21r * d22, z21i = X.z21i * d22, z22 = X.z22 * d22;
-            load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii);
-            load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
-            // _k_update_cols (pointwise.py:136-158) on F, G and Z
+        if (S.stepbad) {
+          status = ST_RANK;
+          break;
+        }
+        // ---- phase C: _k_update_cols / swaps (pointwise.py:178-218)
+        const int flags = S.pflag[warp];
+        bool swap = (flags & 4) != 0;
+        if (flags & 1) {
+          const double z11 = S.px[warp][0], z12r = S.px[warp][1], z12i = S.px[warp][2];
+          const double z21r = S.px[warp][3], z21i = S.px[warp][4], z22 = S.px[warp][5];
+          double zi_[EPL], zii[EPL], zj_[EPL], zji[EPL];
+          load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii);
+          load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
 #define HZG_UPD(yr, yi, yjr_, yji_)                                                         \
   {                                                                                        \
     double yir = yr[e], yjr = yjr_[e];                                                     \
@@ -531,28 +608,22 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
     }                                                                                      \
   }
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-              HZG_UPD(fi, fii, fj, fji);
-              HZG_UPD(gi, gii, gj, gji);
-              HZG_UPD(zi_, zii, zj_, zji);
-            }
-#undef HZG_UPD
-            if (kc.sorting && CPLX) {
-              double q0[EPL], q1[EPL];
-#pragma unroll
-              for (int e = 0; e < EPL; ++e) {
-                q0[e] = nrm_term<CPLX>(fi[e], fii[e]);
-                q1[e] = nrm_term<CPLX>(fj[e], fji[e]);
-              }
-              double ni = lane_tree<EPL>(q0), nj = lane_tree<EPL>(q1);
-              swap = ni < nj;
-            }
-            wrote = true;
-            wapplied += 1;
-            wbig += bg;
+          for (int e = 0; e < EPL; ++e) {
+            HZG_UPD(fi, fii, fj, fji);
+            HZG_UPD(gi, gii, gj, gji);
+            HZG_UPD(zi_, zii, zj_, zji);
           }
-        }
-        if (wrote || swap) {
+#undef HZG_UPD
+          if (kc.sorting && CPLX) {
+            double q0[EPL], q1[EPL];
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) {
+              q0[e] = nrm_term<CPLX>(fi[e], fii[e]);
+              q1[e] = nrm_term<CPLX>(fj[e], fji[e]);
+            }
+            double ni = lane_tree<EPL>(q0), nj = lane_tree<EPL>(q1);
+            swap = ni < nj;
+          }
           const int di = swap ? j : i, dj = swap ? i : j;
           store_col<TW, CPLX>(Ar, Ai, di, lane, fi, fii);
           store_col<TW, CPLX>(Ar, Ai, dj, lane, fj, fji);
@@ -560,28 +631,35 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
           store_col<TW, CPLX>(Br, Bi, dj, lane, gj, gji);
           store_col<TW, CPLX>(Zr, Zi, di, lane, zi_, zii);
           store_col<TW, CPLX>(Zr, Zi, dj, lane, zj_, zji);
+        } else if (swap) {
+          double zi_[EPL], zii[EPL], zj_[EPL], zji[EPL];
+          load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii);
+          load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
+          store_col<TW, CPLX>(Ar, Ai, j, lane, fi, fii);
+          store_col<TW, CPLX>(Ar, Ai, i, lane, fj, fji);
+          store_col<TW, CPLX>(Br, Bi, j, lane, gi, gii);
+          store_col<TW, CPLX>(Br, Bi, i, lane, gj, gji);
+          store_col<TW, CPLX>(Zr, Zi, j, lane, zi_, zii);
+          store_col<TW, CPLX>(Zr, Zi, i, lane, zj_, zji);
         }
-        if (__syncthreads_or(mybad)) {
-          status = ST_RANK;
-          break;
+        __syncthreads();
+        if (prof) {
+          tC += clock64() - c0;
+          ++nstep;
         }
       }
       if (status != ST_OK) break;
-      if (lane == 0) {
-        S.wcnt[warp][0] = wapplied;
-        S.wcnt[warp][1] = wbig;
-      }
-      __syncthreads();
-      int s_cnt = 0, b_cnt = 0;
-      for (int q = 0; q < NW; ++q) {
-        s_cnt += S.wcnt[q][0];
-        b_cnt += S.wcnt[q][1];
-      }
-      __syncthreads();
+      const int s_cnt = S.sw_applied, b_cnt = S.sw_big;
       sweeps += 1;
       if (s_cnt == 0) break;
       total += s_cnt;
       big += b_cnt;
+    }
+    if (prof) {
+      P.io.phase[0] += tA;
+      P.io.phase[1] += tB;
+      P.io.phase[2] += tC;
+      P.io.phase[3] += nstep;
     }
   }
 

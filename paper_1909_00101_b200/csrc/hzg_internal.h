@@ -57,6 +57,7 @@ struct InnerOut {
   double* zt;        // [pair][plane][tw*tw]
   int32_t* ident;    // [pair] 1 -> transform is exactly I (skip postmult, blocked.py:480)
   int32_t* counts;   // [osteps][npairs][4]: total, big, status, inner sweeps
+  long long* phase;  // optional diagnostics (CTA 0, warp 0): cycles in phases A, B, C, #steps
 };
 
 // kernel launchers (hzg_kernels.cu / hzg_dmma.cu)

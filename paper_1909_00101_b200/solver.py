@@ -89,7 +89,23 @@ class DeviceGsvd:
             pass
 
     def init(self):
+        self.sweeps = 0
+        self.total = 0
+        self.big = 0
+        self.converged = False
         _native.check(self.lib.hzg_init_fgz(self.ctx), self.ctx, "prescale")
+
+    def set_timing(self, on=True):
+        _native.check(self.lib.hzg_set_timing(self.ctx, int(bool(on))), self.ctx, "set_timing")
+
+    def kernel_times(self, reset=False):
+        """{kind: (ms, launches)} for kind in grammian / inner / postmult."""
+        ms = np.zeros(3)
+        cnt = np.zeros(3, dtype=np.int64)
+        _native.check(self.lib.hzg_kernel_times(self.ctx, ms.ctypes.data_as(ctypes.c_void_p),
+                                                cnt.ctypes.data_as(ctypes.c_void_p), int(bool(reset))),
+                      self.ctx, "kernel_times")
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(("grammian", "inner", "postmult"))}
 
     def sweep(self):
         tot = ctypes.c_int64(0)
@@ -110,6 +126,15 @@ class DeviceGsvd:
                 self.converged = True
                 break
         return self
+
+    def step_counters(self):
+        """int32 (osteps, npairs, 4): total, big, status, inner sweeps of the last sweep."""
+        cnt = ctypes.c_int64(0)
+        self.lib.hzg_step_counters(self.ctx, None, 0, ctypes.byref(cnt))
+        out = np.zeros(cnt.value, dtype=np.int32)
+        _native.check(self.lib.hzg_step_counters(self.ctx, out.ctypes.data_as(ctypes.c_void_p), out.size,
+                                                 ctypes.byref(cnt)), self.ctx, "step_counters")
+        return out.reshape(-1, self.n // self.cfg.block_width // 2, 4)
 
     def run_steps(self, first, count):
         _native.check(self.lib.hzg_run_steps(self.ctx, first, count), self.ctx, "run_steps")
