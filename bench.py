@@ -48,6 +48,9 @@ def parse():
                     help="cond: config 4 (sigma in [1e-8, 1e8]); gauss: iid Gaussian (config 5)")
     ap.add_argument("--w", type=int, default=16)
     ap.add_argument("--seed", type=int, default=4096)
+    ap.add_argument("--max-sweeps", type=int, default=None,
+                    help="outer sweep cap (default: 30, the reference's; 100 for the ill-conditioned config so "
+                         "the solve runs to convergence)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -231,7 +234,8 @@ def main():
 
     Fr0, Gr0, truth = gen_pair(a, torch, device)
     n = a.n
-    cfg = hz.SolverConfig(block_width=a.w)
+    cap = a.max_sweeps if a.max_sweeps else (100 if a.kind == "cond" else 30)
+    cfg = hz.SolverConfig(block_width=a.w, max_outer_sweeps=cap)
     w = a.w
     padn = (-n) % (2 * w)
     assert padn == 0, "bench uses n divisible by 2w"
@@ -385,6 +389,7 @@ def main():
             "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated on the GPU)",
             "config": {"workload": workload_name(a), "n": n, "block_width": w, "sweeps": sweeps,
+                       "max_outer_sweeps": cap, "converged": bool(dev.converged),
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs larger than L2 (F+G+Z = %.0f MB > 126 MB)" % (3 * n * n * 8 / 1e6),
                        "wall_s_per_solve": ms_max / a.steps / 1e3},

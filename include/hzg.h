@@ -118,6 +118,11 @@ int hzg_step_counters(hzg_ctx* ctx, int32_t* out, int64_t capacity, int64_t* cou
  * products), B (2x2 transforms), C (column updates), plus the step count. */
 int hzg_debug_phases(hzg_ctx* ctx, int32_t enable, int64_t* out4);
 
+/* Self-check of the branch-free FP64 division / square root used by the
+ * 2x2 kernels against the IEEE operators on n random operand pairs:
+ * counts4 = {divisions checked, mismatches, roots checked, mismatches}. */
+int hzg_test_fastmath(int64_t n, uint64_t seed, int64_t* counts4);
+
 const char* hzg_last_error(const hzg_ctx* ctx);
 void hzg_destroy(hzg_ctx* ctx);
 

@@ -25,7 +25,8 @@ class HzgConfig(ctypes.Structure):
 
 EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_init_fgz", "hzg_sweep",
            "hzg_run_steps", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
-           "hzg_step_counters", "hzg_debug_phases", "hzg_last_error", "hzg_destroy")
+           "hzg_step_counters", "hzg_debug_phases", "hzg_test_fastmath", "hzg_last_error",
+           "hzg_destroy")
 
 _lib = None
 _lock = threading.Lock()
@@ -68,6 +69,8 @@ def load(path=LIB_PATH):
         L.hzg_step_counters.restype = ctypes.c_int
         L.hzg_debug_phases.argtypes = [P, I32, P]
         L.hzg_debug_phases.restype = ctypes.c_int
+        L.hzg_test_fastmath.argtypes = [I64, ctypes.c_uint64, P]
+        L.hzg_test_fastmath.restype = ctypes.c_int
         L.hzg_last_error.argtypes = [P]
         L.hzg_last_error.restype = ctypes.c_char_p
         L.hzg_destroy.argtypes = [P]

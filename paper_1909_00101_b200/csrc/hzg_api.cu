@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -27,6 +28,10 @@ struct hzg_ctx {
   int w = 0, tw = 0, nblk = 0;
   int osteps = 0, npairs = 0, isteps = 0;
   bool use_dmma = false;
+  bool wavefront = false;   // schedule in circle-position order (ME)
+  int groups = 1;           // position groups of the wavefront sweep graph
+  std::vector<cudaStream_t> gstreams;
+  std::vector<cudaEvent_t> gevents;  // fork, joins[G], step events [2][G]
   std::vector<int32_t> colpair_host;  // [osteps][npairs][2]
   std::vector<int32_t> itable_host;   // [isteps][tw]
   // device state
@@ -116,6 +121,26 @@ int gen_table(bool mm, int n, std::vector<int32_t>& out) {
   return n;
 }
 
+// ME steps in circle-position order (unsorted rows of strategies.py:59-70)
+int circle_table(int n, std::vector<int32_t>& out) {
+  const int half = n / 2;
+  out.assign((size_t)(n - 1) * half * 2, 0);
+  std::vector<int> others(n - 1);
+  for (int i = 1; i < n; ++i) others[i - 1] = i;
+  for (int st = 0; st < n - 1; ++st) {
+    std::vector<int> line(n);
+    line[0] = 0;
+    for (int i = 1; i < n; ++i) line[i] = others[i - 1];
+    for (int i = 0; i < half; ++i) {
+      int a = line[i], b = line[n - 1 - i];
+      out[((size_t)st * half + i) * 2] = std::min(a, b);
+      out[((size_t)st * half + i) * 2 + 1] = std::max(a, b);
+    }
+    std::rotate(others.rbegin(), others.rbegin() + 1, others.rend());
+  }
+  return n - 1;
+}
+
 int64_t pow2c(int64_t v) {
   int64_t m = 1;
   while (m < v) m <<= 1;
@@ -194,8 +219,8 @@ KernelCfg kernel_cfg(const hzg_ctx* c) {
   return k;
 }
 
-int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr) {
-  StepPairs sp{c->d_colpair, c->npairs};
+int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr, int p0 = 0, int pn = -1) {
+  StepPairs sp{c->d_colpair, c->npairs, p0, pn < 0 ? c->npairs : pn};
   KernelCfg kc = kernel_cfg(c);
   if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
   int rc = c->use_dmma ? launch_gram_dmma(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s)
@@ -215,8 +240,8 @@ int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr)
 
 void accumulate_times(hzg_ctx* c) {
   if (!c->timing || c->tev.empty()) return;
-  for (int st = 0; st < c->osteps; ++st) {
-    cudaEvent_t* e = &c->tev[(size_t)st * 4];
+  for (size_t q = 0; q < c->tev.size() / 4; ++q) {
+    cudaEvent_t* e = &c->tev[q * 4];
     for (int k = 0; k < 3; ++k) {
       float ms = 0.f;
       if (cudaEventElapsedTime(&ms, e[k], e[k + 1]) == cudaSuccess) {
@@ -270,7 +295,17 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   c->npairs = c->nblk / 2;
   c->use_dmma = !cfg->exact && dmma_supported(w);
   std::vector<int32_t> outer;
-  c->osteps = gen_table(cfg->outer_mm != 0, c->nblk, outer);
+  if (cfg->outer_mm) {
+    c->osteps = gen_table(true, c->nblk, outer);
+  } else {
+    // ME pair sets in circle-method position order (strategies.py:59-70
+    // before the per-step sort): pair i of step k is (line[i], line[N-1-i]).
+    // Same pairs as the reference's sorted table; the position order makes
+    // step k+1's pair i depend only on step k's pairs i-1 .. i+1, which the
+    // sweep graph exploits (groups of positions run as a wavefront).
+    c->osteps = circle_table(c->nblk, outer);
+    c->wavefront = true;
+  }
   c->colpair_host.resize((size_t)c->osteps * c->npairs * 2);
   for (size_t e = 0; e < c->colpair_host.size(); ++e) c->colpair_host[e] = outer[e] * w;
   std::vector<int32_t> inner;
@@ -291,6 +326,7 @@ int hzg_set_schedule(hzg_ctx* c, const int32_t* colpairs, int32_t osteps, int32_
   c->osteps = osteps;
   c->npairs = npairs;
   c->colpair_host.assign(colpairs, colpairs + (size_t)osteps * npairs * 2);
+  c->wavefront = false;
   c->qr_slots = std::max(1, std::min(16, npairs));
   return HZG_OK;
 }
@@ -368,17 +404,64 @@ int hzg_init_fgz(hzg_ctx* c) {
   return HZG_OK;
 }
 
+static int choose_groups(const hzg_ctx* c) {
+  if (!c->wavefront) return 1;
+  int g = std::max(1, std::min(8, c->npairs / 16));
+  if (const char* e = std::getenv("HZG_GROUPS")) g = std::max(1, std::min(c->npairs, std::atoi(e)));
+  return g;
+}
+
+// One outer sweep as a CUDA graph.  With G > 1 the pairs of every step are
+// split into G contiguous circle-position groups, each on its own capture
+// stream; group g of step k+1 waits only for groups g-1, g, g+1 of step k
+// (the pairs its blocks come from), so Grammian / postmultiply streaming of
+// some groups overlaps the latency-bound inner solves of others.
 static int build_graph(hzg_ctx* c) {
   cudaError_t e;
+  const int G = c->groups = choose_groups(c);
+  if ((int)c->gstreams.size() < G) {
+    for (int g = (int)c->gstreams.size(); g < G; ++g) {
+      cudaStream_t st;
+      if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(c, e, "cudaStreamCreate");
+      c->gstreams.push_back(st);
+    }
+  }
+  const size_t nev = 1 + (size_t)G + 2 * (size_t)G;
+  while (c->gevents.size() < nev) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(c, e, "cudaEventCreate");
+    c->gevents.push_back(ev);
+  }
+  cudaEvent_t fork = c->gevents[0];
+  cudaEvent_t* join = &c->gevents[1];
+  cudaEvent_t* stepev = &c->gevents[1 + G];  // [2][G]
+  if (c->timing && c->tev.empty()) {
+    c->tev.resize((size_t)c->osteps * G * 4);
+    for (auto& ev : c->tev) cudaEventCreate(&ev);
+  }
   if ((e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
     return cuda_fail(c, e, "begin capture");
   int rc = HZG_OK;
-  if (c->timing && c->tev.empty()) {
-    c->tev.resize((size_t)c->osteps * 4);
-    for (auto& e : c->tev) cudaEventCreate(&e);
+  cudaEventRecord(fork, c->cap);
+  for (int g = 0; g < G; ++g) cudaStreamWaitEvent(c->gstreams[g], fork, 0);
+  for (int st = 0; st < c->osteps && rc == HZG_OK; ++st) {
+    for (int g = 0; g < G && rc == HZG_OK; ++g) {
+      cudaStream_t s = c->gstreams[g];
+      if (st > 0) {
+        if (g > 0) cudaStreamWaitEvent(s, stepev[((st - 1) & 1) * G + g - 1], 0);
+        if (g + 1 < G) cudaStreamWaitEvent(s, stepev[((st - 1) & 1) * G + g + 1], 0);
+      }
+      const int p0 = (int)((int64_t)c->npairs * g / G), p1 = (int)((int64_t)c->npairs * (g + 1) / G);
+      rc = launch_step(c, st, s, c->timing ? &c->tev[((size_t)st * G + g) * 4] : nullptr, p0, p1 - p0);
+      cudaEventRecord(stepev[(st & 1) * G + g], s);
+    }
   }
-  for (int st = 0; st < c->osteps && rc == HZG_OK; ++st)
-    rc = launch_step(c, st, c->cap, c->timing ? &c->tev[(size_t)st * 4] : nullptr);
+  for (int g = 0; g < G; ++g) {
+    cudaEventRecord(join[g], c->gstreams[g]);
+    cudaStreamWaitEvent(c->cap, join[g], 0);
+  }
   if (rc == HZG_OK) rc = launch_counters(c->io.counts, (int64_t)c->osteps * c->npairs, c->d_ctr, c->cap);
   if (rc == HZG_OK)
     rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 0, nullptr, nullptr, nullptr, c->d_ctr, c->d_status,
@@ -494,7 +577,7 @@ int hzg_test_block(int32_t tw, int32_t is_complex, const hzg_config* cfg, double
   gw.smax = 1;
   gw.chunk[0] = gw.chunk[1] = 1;
   InnerOut io{d_zt, d_misc, d_misc + 4, nullptr};
-  StepPairs sp{d_misc + 8, 1};  // colpair (0, w): only used by the QR fallback
+  StepPairs sp{d_misc + 8, 1, 0, 1};  // colpair (0, 0): only used by the QR fallback
   KernelCfg kc = kernel_cfg(&c);
   kc.fallback_qr = 0;  // the block test has no columns to shorten
   Plane dummy{nullptr, nullptr, 0, 0};
@@ -558,6 +641,11 @@ int hzg_debug_phases(hzg_ctx* c, int32_t enable, int64_t* out4) {
   return HZG_OK;
 }
 
+int hzg_test_fastmath(int64_t n, uint64_t seed, int64_t* counts4) {
+  if (!counts4 || n < 1) return HZG_INVALID;
+  return fastmath_check(n, seed, counts4);
+}
+
 const char* hzg_last_error(const hzg_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 void hzg_destroy(hzg_ctx* c) {
@@ -567,6 +655,8 @@ void hzg_destroy(hzg_ctx* c) {
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   for (auto& e : c->tev) cudaEventDestroy(e);
+  for (auto& e : c->gevents) cudaEventDestroy(e);
+  for (auto& s : c->gstreams) cudaStreamDestroy(s);
   delete c;
 }
 

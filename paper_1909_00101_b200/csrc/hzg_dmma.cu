@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(GramCfg<TW, CPLX>::NWARP * 32) k_gram_dmma(Gra
   double* stages = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::NS * C::STAGE * sizeof(double));
 
-  const int pair = blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
   if (split >= P.gw.nsplit[mat]) return;
   const Plane& Y = P.Y[mat];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(PostCfg<TW, CPLX>::NWARP * 32) k_post_dmma(Pos
   using C = PostCfg<TW, CPLX>;
   constexpr int NP = C::NP;
   constexpr int w = TW / 2;
-  const int pair = blockIdx.x, mat = blockIdx.y;
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y;
   if (P.io.ident[pair]) return;
   const Plane& Y = P.Y[mat];
   const int64_t rbeg = (int64_t)blockIdx.z * P.chunk;
@@ -348,7 +348,7 @@ int gram_t(const GramParams& p, cudaStream_t s) {
     set_smem(k_gram_dmma<TW, CPLX>, C::SMEM);
     once = true;
   }
-  dim3 grid(p.sp.npairs, 2, p.gw.smax);
+  dim3 grid(p.sp.pn, 2, p.gw.smax);
   k_gram_dmma<TW, CPLX><<<grid, C::NWARP * 32, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
@@ -361,7 +361,7 @@ int post_t(const PostParams& p, int64_t mmax, cudaStream_t s) {
     set_smem(k_post_dmma<TW, CPLX>, C::SMEM);
     once = true;
   }
-  dim3 grid(p.sp.npairs, 3, (unsigned)((mmax + p.chunk - 1) / p.chunk));
+  dim3 grid(p.sp.pn, 3, (unsigned)((mmax + p.chunk - 1) / p.chunk));
   k_post_dmma<TW, CPLX><<<grid, C::NWARP * 32, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

@@ -290,6 +290,34 @@ __device__ int block_qr(const Plane& Y, int64_t c0, int64_t c1, int w, double* S
 #undef SI_
 }
 
+// _k_process_pivot's scalar part (pointwise.py:165-207) for one pivot:
+// q = {a11, a22, a12r, b11, b22, b12r, a12i, b12i}.  Returns flags (1 applied,
+// 2 big, 4 swap, 8 bad) and, when applied, the rescaled Z-hat entries.
+template <bool CPLX, class M>
+__device__ __forceinline__ int pivot_scalar(M& m, const KernelCfg& kc, const double* q, double (&z)[6]) {
+  double a11 = q[0], a22 = q[1], a12r = q[2], b11 = q[3], b22 = q[4], b12r = q[5];
+  double a12i = CPLX ? q[6] : 0.0, b12i = CPLX ? q[7] : 0.0;
+  if (!(a11 > 0.0 && a22 > 0.0 && b11 > 0.0 && b22 > 0.0)) return 8;
+  double d11 = 1.0, d22 = 1.0;
+  if (kc.per_step_rescale) rescale2(m, a11, a12r, a12i, a22, b11, b12r, b12i, b22, d11, d22);
+  if (gate<CPLX>(m, a11, a12r, a12i, a22, b12r, b12i, kc.epsn)) return (kc.sorting && a11 < a22) ? 4 : 0;
+  Xform X = transform<CPLX>(m, a11, a12r, a12i, a22, b12r, b12i);
+  const int bg = kc.crit_c2 ? !(X.cphi == 1.0 && X.cpsi == 1.0) : !(X.z11 == 1.0 && X.z22 == 1.0);
+  int flags = 1 | (bg ? 2 : 0);
+  if (kc.sorting && !CPLX) {
+    double a1pp, a2pp;
+    diag_after_real(X.z11, X.z12r, X.z21r, X.z22, a11, a12r, a22, a1pp, a2pp);
+    if (a1pp < a2pp) flags |= 4;
+  }
+  z[0] = X.z11 * d11;
+  z[1] = X.z12r * d11;
+  z[2] = X.z12i * d11;
+  z[3] = X.z21r * d22;
+  z[4] = X.z21i * d22;
+  z[5] = X.z22 * d22;
+  return flags;
+}
+
 struct InnerParams {
   Plane F, G;
   StepPairs sp;
@@ -311,7 +339,7 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
   constexpr int NP = CPLX ? 2 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<InnerSmem<TW, CPLX>*>(smem_raw);
-  const int pair = blockIdx.x;
+  const int pair = P.sp.p0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = blockDim.x;
   const KernelCfg& kc = P.kc;
@@ -525,35 +553,19 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
         if (warp == 0) {
           int flags = 0;  // 1 applied, 2 big, 4 swap, 8 bad
           if (lane < NW) {
-            double a11 = S.pd[lane][0], a22 = S.pd[lane][1], a12r = S.pd[lane][2], b11 = S.pd[lane][3];
-            double b22 = S.pd[lane][4], b12r = S.pd[lane][5];
-            double a12i = CPLX ? S.pd[lane][6] : 0.0, b12i = CPLX ? S.pd[lane][7] : 0.0;
-            if (!(a11 > 0.0 && a22 > 0.0 && b11 > 0.0 && b22 > 0.0)) {
-              flags = 8;
-            } else {
-              double d11 = 1.0, d22 = 1.0;
-              if (kc.per_step_rescale) rescale2(a11, a12r, a12i, a22, b11, b12r, b12i, b22, d11, d22);
-              if (gate(a11, a12r, a12i, a22, b12r, b12i, kc.epsn)) {
-                if (kc.sorting && a11 < a22) flags = 4;
-              } else {
-                Xform X = CPLX ? transform_cplx(a11, a12r, a12i, a22, b12r, b12i)
-                               : transform_real(a11, a12r, a22, b12r);
-                int bg = kc.crit_c2 ? !(X.cphi == 1.0 && X.cpsi == 1.0) : !(X.z11 == 1.0 && X.z22 == 1.0);
-                flags = 1 | (bg ? 2 : 0);
-                if (kc.sorting && !CPLX) {
-                  double a1pp, a2pp;
-                  diag_after_real(X.z11, X.z12r, X.z21r, X.z22, a11, a12r, a22, a1pp, a2pp);
-                  if (a1pp < a2pp) flags |= 4;
-                }
-                S.px[lane][0] = X.z11 * d11;
-                S.px[lane][1] = X.z12r * d11;
-                S.px[lane][2] = X.z12i * d11;
-                S.px[lane][3] = X.z21r * d22;
-                S.px[lane][4] = X.z21i * d22;
-                S.px[lane][5] = X.z22 * d22;
-                lane_applied += 1;
-                lane_big += bg;
-              }
+            const double* q = S.pd[lane];
+            double z[6];
+            FastMath fm;
+            flags = pivot_scalar<CPLX>(fm, kc, q, z);
+            if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
+              IeeeMath im;
+              flags = pivot_scalar<CPLX>(im, kc, q, z);
+            }
+            if (flags & 1) {
+#pragma unroll
+              for (int c = 0; c < 6; ++c) S.px[lane][c] = z[c];
+              lane_applied += 1;
+              lane_big += (flags >> 1) & 1;
             }
             S.pflag[lane] = flags;
           }
@@ -723,7 +735,7 @@ int launch_inner_t(const InnerParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(k_inner<TW, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_done = true;
   }
-  k_inner<TW, CPLX><<<p.sp.npairs, TW / 2 * 32, smem, s>>>(p);
+  k_inner<TW, CPLX><<<p.sp.pn, TW / 2 * 32, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

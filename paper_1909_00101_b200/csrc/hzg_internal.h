@@ -28,7 +28,8 @@ struct Plane {
 // with the smaller logical index (the reference's sorted (p, q), blocked.py:438-439).
 struct StepPairs {
   const int32_t* colpair;  // [osteps][npairs][2]
-  int npairs;
+  int npairs;              // pairs per step (row stride of colpair)
+  int p0, pn;              // the pair range [p0, p0 + pn) this launch processes
 };
 
 struct KernelCfg {
@@ -83,5 +84,6 @@ int launch_finalize(const Plane& U, const Plane& V, const Plane& Z, int64_t n, i
                     cudaStream_t s);
 
 bool dmma_supported(int w);
+int fastmath_check(int64_t n, uint64_t seed, int64_t* out4);
 
 }  // namespace hzg

@@ -139,7 +139,7 @@ struct GramExactParams {
 };
 
 __global__ void __launch_bounds__(256) k_gram_exact(GramExactParams P) {
-  const int pair = blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (split >= P.gw.nsplit[mat]) return;
   const Plane& Y = P.Y[mat];
@@ -199,7 +199,7 @@ struct PostExactParams {
 
 template <int TW, bool CPLX>
 __global__ void __launch_bounds__(128) k_postmult_exact(PostExactParams P) {
-  const int pair = blockIdx.y, mat = blockIdx.z;
+  const int pair = P.sp.p0 + blockIdx.y, mat = blockIdx.z;
   if (P.io.ident[pair]) return;
   constexpr int NP = CPLX ? 2 : 1;
   extern __shared__ double zt_raw[];
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(128) k_postmult_exact(PostExactParams P) {
 
 template <int TW, bool CPLX>
 int launch_post_exact_t(const PostExactParams& p, int64_t mmax, cudaStream_t s) {
-  dim3 grid((unsigned)((mmax + 127) / 128), p.sp.npairs, 3);
+  dim3 grid((unsigned)((mmax + 127) / 128), p.sp.pn, 3);
   const size_t smem = (CPLX ? 2 : 1) * TW * TW * sizeof(double);
   static bool once = false;
   if (!once) {
@@ -378,7 +378,51 @@ __global__ void k_gather(GatherParams P) {
   }
 }
 
+// self-check of the branch-free division / square root against the IEEE
+// operators on random operands spanning the whole exponent range
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_fastmath_check(int64_t n, uint64_t seed, unsigned long long* cnt) {
+  unsigned long long c[4] = {0, 0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h1 = mix64(seed + 2 * i + 1), h2 = mix64(seed + 2 * i + 2);
+    // random mantissas; exponents mostly moderate, sometimes anywhere
+    uint64_t e1 = (h1 >> 52) & 0x7ff, e2 = (h2 >> 52) & 0x7ff;
+    if ((h1 & 3) != 0) e1 = 1023 + ((int)(e1 % 120) - 60);
+    if ((h2 & 3) != 0) e2 = 1023 + ((int)(e2 % 120) - 60);
+    double a = __longlong_as_double((long long)(((h1 & 0x000fffffffffffffull)) | (e1 << 52) | (h1 & (1ull << 63) ? (1ull << 63) : 0)));
+    double b = __longlong_as_double((long long)(((h2 & 0x000fffffffffffffull)) | (e2 << 52)));
+    bool ok = true;
+    double q = fast_div(a, b, ok);
+    if (ok) {
+      ++c[0];
+      if (__double_as_longlong(q) != __double_as_longlong(a / b)) ++c[1];
+    }
+    ok = true;
+    double r = fast_sqrt(b, ok);
+    if (ok) {
+      ++c[2];
+      if (__double_as_longlong(r) != __double_as_longlong(sqrt(b))) ++c[3];
+    }
+  }
+  for (int k = 0; k < 4; ++k) atomicAdd(&cnt[k], c[k]);
+}
+
 }  // namespace
+
+int fastmath_check(int64_t n, uint64_t seed, int64_t* out4) {
+  unsigned long long* d = nullptr;
+  cudaMalloc(&d, 32);
+  cudaMemset(d, 0, 32);
+  k_fastmath_check<<<148 * 8, 256>>>(n, seed, d);
+  cudaError_t e = cudaMemcpy(out4, d, 32, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? 0 : 3;
+}
 
 int launch_prescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, int cplx, int do_prescale,
                     int32_t* status, cudaStream_t s) {
@@ -397,7 +441,7 @@ int launch_rescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, in
 int launch_gram_exact(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
                       const GramWS& gw, cudaStream_t s) {
   GramExactParams p{{F, G}, sp, step, w, cplx, gw};
-  dim3 grid(sp.npairs, 2, gw.smax);
+  dim3 grid(sp.pn, 2, gw.smax);
   k_gram_exact<<<grid, 256, 0, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

@@ -124,6 +124,15 @@ def test_inner_block_kernel_not_pd_signal():
     assert cnt[2] == 2
 
 
+def test_fast_div_sqrt_bitwise():
+    """The branch-free division / square root of the 2x2 kernels equal the
+    IEEE operators bitwise wherever their range check admits them."""
+    out = np.zeros(4, dtype=np.int64)
+    assert _native.load().hzg_test_fastmath(100_000_000, 12345, out.ctypes.data_as(ctypes.c_void_p)) == 0
+    assert out[0] > 0.9e8 and out[2] > 0.9e8
+    assert out[1] == 0 and out[3] == 0, out
+
+
 # ---------------------------------------------------------------------------
 # DMMA mode: tolerance parity + reproducibility
 # ---------------------------------------------------------------------------
