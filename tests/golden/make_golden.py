@@ -55,6 +55,22 @@ def cases(hz):
     g = gaussian_stream(2024, 2 * 200 * 200)
     add("gauss200_w16", g[:40000].reshape((200, 200), order="F"), g[40000:].reshape((200, 200), order="F"),
         full=False, block_width=16)
+    # nearly dependent F columns: block Grammians fail Cholesky, the QR
+    # shortening fallback takes over (blocked.py:450-462; test_blocked.py:213-230)
+    def dependent(n, seed, eps=1e-9, cplx=False):
+        rng = np.random.default_rng(seed)
+        base = rng.standard_normal(n) + (1j * rng.standard_normal(n) if cplx else 0)
+        F = np.empty((n, n), dtype=complex if cplx else float)
+        for j in range(n):
+            F[:, j] = base + eps * rng.standard_normal(n)
+        G = np.eye(n) + 1e-3 * rng.standard_normal((n, n))
+        if cplx:
+            G = G + 1e-3j * rng.standard_normal((n, n))
+        return F, G
+    add("qrfallback8_w2", *dependent(8, 31), block_width=2)
+    add("qrfallback64_w16", *dependent(64, 7), block_width=16)
+    add("qrfallback64_w8", *dependent(64, 7), block_width=8)
+    add("qrfallback48_complex_w8", *dependent(48, 11, cplx=True), block_width=8)
     pair, _ = hz.gen_pair(hz.random_genspec(256, 4242, "real"))
     add("genpair256_w16", pair.F.to_dense(), pair.G.to_dense(), full=False, block_width=16)
     return out
