@@ -12,6 +12,7 @@
 // counters are bitwise those of the reference's _block_task
 // (blocked.py:435-484; pointwise.py:161-293).
 #include <cstdio>
+#include <cstdlib>
 
 #include "hzg_device.cuh"
 #include "hzg_internal.h"
@@ -332,9 +333,10 @@ struct InnerParams {
   int32_t* qr_locks;
 };
 
-template <int TW, bool CPLX>
-__global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
-  constexpr int NW = TW / 2;
+template <int TW, bool CPLX, int PPW>
+__global__ void __launch_bounds__(TW / 2 / PPW * 32) k_inner(InnerParams P) {
+  constexpr int NPIV = TW / 2;      // pivots per inner step
+  constexpr int NW = NPIV / PPW;    // warps: each forms / applies PPW pivots
   constexpr int EPL = Lanes<TW>::EPL;
   constexpr int NP = CPLX ? 2 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -490,30 +492,38 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
       int lane_applied = 0, lane_big = 0;  // warp 0, lane p: pivot p's counts this sweep
       for (int st = 0; st < P.isteps; ++st) {
         if (prof) c0 = clock64();
-        const int i = S.tab[(st * NW + warp) * 2];
-        const int j = S.tab[(st * NW + warp) * 2 + 1];
-        // ---- phase A
-        double fi[EPL], fii[EPL], fj[EPL], fji[EPL], gi[EPL], gii[EPL], gj[EPL], gji[EPL];
-        load_col<TW, CPLX>(Ar, Ai, i, lane, fi, fii);
-        load_col<TW, CPLX>(Ar, Ai, j, lane, fj, fji);
-        load_col<TW, CPLX>(Br, Bi, i, lane, gi, gii);
-        load_col<TW, CPLX>(Br, Bi, j, lane, gj, gji);
-        {
+        // ---- phase A (pivot pv = warp + k * NW, k < PPW)
+        int ii[PPW], jj[PPW];
+        double fi[PPW][EPL], fii[PPW][EPL], fj[PPW][EPL], fji[PPW][EPL];
+        double gi[PPW][EPL], gii[PPW][EPL], gj[PPW][EPL], gji[PPW][EPL];
+#pragma unroll
+        for (int k = 0; k < PPW; ++k) {
+          const int pv = warp + k * NW;
+          ii[k] = S.tab[(st * NPIV + pv) * 2];
+          jj[k] = S.tab[(st * NPIV + pv) * 2 + 1];
+          load_col<TW, CPLX>(Ar, Ai, ii[k], lane, fi[k], fii[k]);
+          load_col<TW, CPLX>(Ar, Ai, jj[k], lane, fj[k], fji[k]);
+          load_col<TW, CPLX>(Br, Bi, ii[k], lane, gi[k], gii[k]);
+          load_col<TW, CPLX>(Br, Bi, jj[k], lane, gj[k], gji[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < PPW; ++k) {
+          const int pv = warp + k * NW;
           double p[8][EPL];
 #pragma unroll
           for (int e = 0; e < EPL; ++e) {
-            p[0][e] = nrm_term<CPLX>(fi[e], fii[e]);
-            p[1][e] = nrm_term<CPLX>(fj[e], fji[e]);
-            p[3][e] = nrm_term<CPLX>(gi[e], gii[e]);
-            p[4][e] = nrm_term<CPLX>(gj[e], gji[e]);
+            p[0][e] = nrm_term<CPLX>(fi[k][e], fii[k][e]);
+            p[1][e] = nrm_term<CPLX>(fj[k][e], fji[k][e]);
+            p[3][e] = nrm_term<CPLX>(gi[k][e], gii[k][e]);
+            p[4][e] = nrm_term<CPLX>(gj[k][e], gji[k][e]);
             if (CPLX) {
-              p[2][e] = dot_re_term(fi[e], fii[e], fj[e], fji[e]);
-              p[6][e] = dot_im_term(fi[e], fii[e], fj[e], fji[e]);
-              p[5][e] = dot_re_term(gi[e], gii[e], gj[e], gji[e]);
-              p[7][e] = dot_im_term(gi[e], gii[e], gj[e], gji[e]);
+              p[2][e] = dot_re_term(fi[k][e], fii[k][e], fj[k][e], fji[k][e]);
+              p[6][e] = dot_im_term(fi[k][e], fii[k][e], fj[k][e], fji[k][e]);
+              p[5][e] = dot_re_term(gi[k][e], gii[k][e], gj[k][e], gji[k][e]);
+              p[7][e] = dot_im_term(gi[k][e], gii[k][e], gj[k][e], gji[k][e]);
             } else {
-              p[2][e] = fi[e] * fj[e];
-              p[5][e] = gi[e] * gj[e];
+              p[2][e] = fi[k][e] * fj[k][e];
+              p[5][e] = gi[k][e] * gj[k][e];
               p[6][e] = 0.0;
               p[7][e] = 0.0;
             }
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
           double s1 = (b2 ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? s2[0] : s2[1], 4);
           s1 = s1 + __shfl_xor_sync(0xffffffffu, s1, 8);
           s1 = s1 + __shfl_xor_sync(0xffffffffu, s1, 16);
-          if (lane < 8) S.pd[warp][4 * b0 + 2 * b1 + b2] = s1;
+          if (lane < 8) S.pd[pv][4 * b0 + 2 * b1 + b2] = s1;
         }
         __syncthreads();
         if (prof) {
@@ -552,7 +562,7 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
         // ---- phase B: _k_process_pivot's scalar part (pointwise.py:165-207)
         if (warp == 0) {
           int flags = 0;  // 1 applied, 2 big, 4 swap, 8 bad
-          if (lane < NW) {
+          if (lane < NPIV) {
             const double* q = S.pd[lane];
             double z[6];
             FastMath fm;
@@ -595,14 +605,20 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
           break;
         }
         // ---- phase C: _k_update_cols / swaps (pointwise.py:178-218)
-        const int flags = S.pflag[warp];
-        bool swap = (flags & 4) != 0;
-        if (flags & 1) {
-          const double z11 = S.px[warp][0], z12r = S.px[warp][1], z12i = S.px[warp][2];
-          const double z21r = S.px[warp][3], z21i = S.px[warp][4], z22 = S.px[warp][5];
+#pragma unroll
+        for (int k = 0; k < PPW; ++k) {
+          const int pv = warp + k * NW;
+          const int i = ii[k], j = jj[k];
+          const int flags = S.pflag[pv];
+          bool swap = (flags & 4) != 0;
           double zi_[EPL], zii[EPL], zj_[EPL], zji[EPL];
-          load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii);
-          load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
+          if (flags & 5) {
+            load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii);
+            load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
+          }
+          if (flags & 1) {
+            const double z11 = S.px[pv][0], z12r = S.px[pv][1], z12i = S.px[pv][2];
+            const double z21r = S.px[pv][3], z21i = S.px[pv][4], z22 = S.px[pv][5];
 #define HZG_UPD(yr, yi, yjr_, yji_)                                                         \
   {                                                                                        \
     double yir = yr[e], yjr = yjr_[e];                                                     \
@@ -620,39 +636,32 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
     }                                                                                      \
   }
 #pragma unroll
-          for (int e = 0; e < EPL; ++e) {
-            HZG_UPD(fi, fii, fj, fji);
-            HZG_UPD(gi, gii, gj, gji);
-            HZG_UPD(zi_, zii, zj_, zji);
-          }
-#undef HZG_UPD
-          if (kc.sorting && CPLX) {
-            double q0[EPL], q1[EPL];
-#pragma unroll
             for (int e = 0; e < EPL; ++e) {
-              q0[e] = nrm_term<CPLX>(fi[e], fii[e]);
-              q1[e] = nrm_term<CPLX>(fj[e], fji[e]);
+              HZG_UPD(fi[k], fii[k], fj[k], fji[k]);
+              HZG_UPD(gi[k], gii[k], gj[k], gji[k]);
+              HZG_UPD(zi_, zii, zj_, zji);
             }
-            double ni = lane_tree<EPL>(q0), nj = lane_tree<EPL>(q1);
-            swap = ni < nj;
+#undef HZG_UPD
+            if (kc.sorting && CPLX) {
+              double q0[EPL], q1[EPL];
+#pragma unroll
+              for (int e = 0; e < EPL; ++e) {
+                q0[e] = nrm_term<CPLX>(fi[k][e], fii[k][e]);
+                q1[e] = nrm_term<CPLX>(fj[k][e], fji[k][e]);
+              }
+              double ni = lane_tree<EPL>(q0), nj = lane_tree<EPL>(q1);
+              swap = ni < nj;
+            }
           }
-          const int di = swap ? j : i, dj = swap ? i : j;
-          store_col<TW, CPLX>(Ar, Ai, di, lane, fi, fii);
-          store_col<TW, CPLX>(Ar, Ai, dj, lane, fj, fji);
-          store_col<TW, CPLX>(Br, Bi, di, lane, gi, gii);
-          store_col<TW, CPLX>(Br, Bi, dj, lane, gj, gji);
-          store_col<TW, CPLX>(Zr, Zi, di, lane, zi_, zii);
-          store_col<TW, CPLX>(Zr, Zi, dj, lane, zj_, zji);
-        } else if (swap) {
-          double zi_[EPL], zii[EPL], zj_[EPL], zji[EPL];
-          load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii);
-          load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
-          store_col<TW, CPLX>(Ar, Ai, j, lane, fi, fii);
-          store_col<TW, CPLX>(Ar, Ai, i, lane, fj, fji);
-          store_col<TW, CPLX>(Br, Bi, j, lane, gi, gii);
-          store_col<TW, CPLX>(Br, Bi, i, lane, gj, gji);
-          store_col<TW, CPLX>(Zr, Zi, j, lane, zi_, zii);
-          store_col<TW, CPLX>(Zr, Zi, i, lane, zj_, zji);
+          if (flags & 1 || swap) {
+            const int di = swap ? j : i, dj = swap ? i : j;
+            store_col<TW, CPLX>(Ar, Ai, di, lane, fi[k], fii[k]);
+            store_col<TW, CPLX>(Ar, Ai, dj, lane, fj[k], fji[k]);
+            store_col<TW, CPLX>(Br, Bi, di, lane, gi[k], gii[k]);
+            store_col<TW, CPLX>(Br, Bi, dj, lane, gj[k], gji[k]);
+            store_col<TW, CPLX>(Zr, Zi, di, lane, zi_, zii);
+            store_col<TW, CPLX>(Zr, Zi, dj, lane, zj_, zji);
+          }
         }
         __syncthreads();
         if (prof) {
@@ -729,13 +738,28 @@ __global__ void __launch_bounds__(TW / 2 * 32) k_inner(InnerParams P) {
 
 template <int TW, bool CPLX>
 int launch_inner_t(const InnerParams& p, cudaStream_t s) {
-  size_t smem = sizeof(InnerSmem<TW, CPLX>);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_inner<TW, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_done = true;
+  // pivots per warp in the dot / update phases (HZG_PPW overrides, for tuning)
+  constexpr int kPPW = 1;  // measured best at w = 16 (profiles/r01_notes.md)
+  static int ppw = -1;
+  if (ppw < 0) {
+    ppw = kPPW;
+    if (const char* e = std::getenv("HZG_PPW")) ppw = std::atoi(e);
+    if (ppw != 1 && ppw != 2 && ppw != 4) ppw = kPPW;
+    if (TW / 2 < ppw) ppw = 1;
   }
-  k_inner<TW, CPLX><<<p.sp.pn, TW / 2 * 32, smem, s>>>(p);
+  size_t smem = sizeof(InnerSmem<TW, CPLX>);
+  auto launch = [&](auto kern, int ppw_) {
+    static bool attr_done = false;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    (void)attr_done;
+    kern<<<p.sp.pn, TW / 2 / ppw_ * 32, smem, s>>>(p);
+  };
+  if (ppw == 4 && TW / 2 >= 4)
+    launch(k_inner<TW, CPLX, (TW / 2 >= 4 ? 4 : 1)>, TW / 2 >= 4 ? 4 : 1);
+  else if (ppw == 2 && TW / 2 >= 2)
+    launch(k_inner<TW, CPLX, (TW / 2 >= 2 ? 2 : 1)>, TW / 2 >= 2 ? 2 : 1);
+  else
+    launch(k_inner<TW, CPLX, 1>, 1);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
