@@ -167,7 +167,7 @@ void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
     chunk = std::max<int64_t>(32, std::min<int64_t>(P, 2048));
     nsplit = (int)std::max<int64_t>(1, P / chunk);
   } else {
-    chunk = 1024;
+    chunk = 512;
     nsplit = (int)pow2c((m + chunk - 1) / chunk);
   }
 }

@@ -190,6 +190,130 @@ __global__ void __launch_bounds__(GramCfg<TW, CPLX>::NWARP * 32) k_gram_dmma(Gra
 }
 
 // ---------------------------------------------------------------------------
+// Grammian partials, k-split form (2w <= 32).  Every warp keeps all upper
+// 8x8 tiles in registers and takes an interleaved quarter of the k-steps of
+// each 64-row tile (complex: warps 0-1 the real plane, 2-3 the imaginary
+// plane, each half of the k-steps), so the DMMA work is split evenly over the
+// four SM sub-partitions; the per-warp partial sums are folded in a fixed
+// order through shared memory at the end.
+// ---------------------------------------------------------------------------
+template <int TW, bool CPLX>
+struct GramKsCfg {
+  static constexpr int NT = TW / 8;
+  static constexpr int NTILE = NT * (NT + 1) / 2;
+  static constexpr int NWARP = 4;
+  static constexpr int NP = CPLX ? 2 : 1;
+  static constexpr int NS = 3;
+  static constexpr int KSTRIDE = CPLX ? 2 : 4;  // warps sharing one plane's k-steps
+  static constexpr size_t STAGE = (size_t)NP * TW * kRS;
+  static constexpr size_t RED = (size_t)NWARP * NTILE * 64;  // doubles
+  static constexpr size_t BUF = NS * STAGE > RED ? NS * STAGE : RED;
+  static constexpr size_t SMEM = BUF * sizeof(double) + 64;
+};
+
+template <int TW, bool CPLX>
+__global__ void __launch_bounds__(128) k_gram_ks(GramParams P) {
+  using C = GramKsCfg<TW, CPLX>;
+  constexpr int NP = C::NP, NT = C::NT, NTILE = C::NTILE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stages = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BUF * sizeof(double));
+
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
+  if (split >= P.gw.nsplit[mat]) return;
+  const Plane& Y = P.Y[mat];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int plane = CPLX ? (warp >> 1) : 0;
+  const int ks0 = CPLX ? (warp & 1) : warp;
+  const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
+  const int64_t L = P.gw.chunk[mat];
+  const int64_t rbeg = (int64_t)split * L;
+  const int64_t rend = rbeg + L < Y.rows ? rbeg + L : Y.rows;
+  const int ntiles = rend > rbeg ? (int)((rend - rbeg + kR - 1) / kR) : 0;
+
+  if (tid == 0) {
+    for (int q = 0; q < C::NS; ++q) mbar_init(&full[q], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int q = 0; q < C::NS && q < ntiles; ++q) {
+      int64_t r0 = rbeg + (int64_t)q * kR;
+      int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+      issue_tile_load<TW, NP>(Y, cp, r0, nv, stages + q * C::STAGE, &full[q], lane);
+    }
+
+  double acc[NTILE][2];
+#pragma unroll
+  for (int q = 0; q < NTILE; ++q) acc[q][0] = acc[q][1] = 0.0;
+
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % C::NS;
+    mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
+    const double* st = stages + s * C::STAGE;
+    const int64_t r0 = rbeg + (int64_t)it * kR;
+    const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+#pragma unroll
+    for (int ks = ks0; ks < kR / 4; ks += C::KSTRIDE) {
+      const int k = ks * 4 + t;
+      const bool ok = k < nv;
+      double fr[NT], fi[NT];
+#pragma unroll
+      for (int cg = 0; cg < NT; ++cg) {
+        fr[cg] = ok ? st[(size_t)(cg * 8 + g) * kRS + k] : 0.0;
+        fi[cg] = (CPLX && ok) ? st[(size_t)(TW + cg * 8 + g) * kRS + k] : 0.0;
+      }
+      int q = 0;
+#pragma unroll
+      for (int I = 0; I < NT; ++I)
+#pragma unroll
+        for (int J = I; J < NT; ++J, ++q) {
+          if (!CPLX) {
+            dmma884(acc[q][0], acc[q][1], fr[I], fr[J]);
+          } else if (plane == 0) {  // Re = ar br + ai bi
+            dmma884(acc[q][0], acc[q][1], fr[I], fr[J]);
+            dmma884(acc[q][0], acc[q][1], fi[I], fi[J]);
+          } else {  // Im = ar bi - ai br
+            dmma884(acc[q][0], acc[q][1], fr[I], fi[J]);
+            dmma884(acc[q][0], acc[q][1], -fi[I], fr[J]);
+          }
+        }
+    }
+    __syncthreads();
+    if (warp == 0 && it + C::NS < ntiles) {
+      int64_t r1 = rbeg + (int64_t)(it + C::NS) * kR;
+      int nv1 = (int)(rend - r1 < kR ? rend - r1 : kR);
+      issue_tile_load<TW, NP>(Y, cp, r1, nv1, stages + s * C::STAGE, &full[s], lane);
+    }
+  }
+  // fold the per-warp partials in a fixed order
+  double* red = stages;  // all bulk loads have landed and been consumed
+#pragma unroll
+  for (int q = 0; q < NTILE; ++q) {
+    red[((size_t)warp * NTILE + q) * 64 + lane * 2] = acc[q][0];
+    red[((size_t)warp * NTILE + q) * 64 + lane * 2 + 1] = acc[q][1];
+  }
+  __syncthreads();
+  double* out = P.gw.part + (((int64_t)pair * 2 + mat) * P.gw.smax + split) * NP * TW * TW;
+  for (int e = tid; e < NP * NTILE * 64; e += blockDim.x) {
+    const int pl = e / (NTILE * 64), rem = e % (NTILE * 64), q = rem / 64, l = (rem % 64) / 2, h = rem % 2;
+    double v = 0.0;
+#pragma unroll
+    for (int wv = 0; wv < C::KSTRIDE; ++wv) v += red[((size_t)(pl * C::KSTRIDE + wv) * NTILE + q) * 64 + l * 2 + h];
+    // tile q -> (I, J)
+    int I = 0, qq = q;
+    while (qq >= NT - I) {
+      qq -= NT - I;
+      ++I;
+    }
+    const int J = I + qq;
+    const int r = I * 8 + (l >> 2), c = J * 8 + 2 * (l & 3) + h;
+    out[(size_t)pl * TW * TW + (size_t)c * TW + r] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Postmultiply [Y_p Y_q] <- [Y_p Y_q] Z~ for F, G and Z.  4 warps along the
 // 64 rows (16 rows each) x WN warps along the columns (32 columns each).
 // ---------------------------------------------------------------------------
@@ -335,6 +459,263 @@ __global__ void __launch_bounds__(PostCfg<TW, CPLX>::NWARP * 32) k_post_dmma(Pos
   if (warp == 0) bulk_wait_all<0>();
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialized streaming kernels (2w <= 32): warp 4 is the TMA producer
+// (bulk loads, and for the postmultiply the bulk stores), warps 0-3 compute.
+// Stages are handed over with mbarriers only -- no CTA-wide barrier inside
+// the tile loop -- so DMMA work, loads and stores of different tiles overlap.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void consumer_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+template <int TW, bool CPLX>
+struct GramWsCfg {
+  static constexpr int NT = TW / 8;
+  static constexpr int NTILE = NT * (NT + 1) / 2;
+  static constexpr int NP = CPLX ? 2 : 1;
+  static constexpr int NS = 4;
+  static constexpr int KSTRIDE = CPLX ? 2 : 4;
+  static constexpr size_t STAGE = (size_t)NP * TW * kRS;
+  static constexpr size_t RED = (size_t)4 * NTILE * 64;
+  static constexpr size_t BUF = NS * STAGE > RED ? NS * STAGE : RED;
+  static constexpr size_t SMEM = BUF * sizeof(double) + 2 * NS * 8 + 64;
+};
+
+template <int TW, bool CPLX>
+__global__ void __launch_bounds__(160) k_gram_ws(GramParams P) {
+  using C = GramWsCfg<TW, CPLX>;
+  constexpr int NP = C::NP, NT = C::NT, NTILE = C::NTILE;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stages = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BUF * sizeof(double));
+  uint64_t* empty = full + C::NS;
+
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
+  if (split >= P.gw.nsplit[mat]) return;
+  const Plane& Y = P.Y[mat];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
+  const int64_t L = P.gw.chunk[mat];
+  const int64_t rbeg = (int64_t)split * L;
+  const int64_t rend = rbeg + L < Y.rows ? rbeg + L : Y.rows;
+  const int ntiles = rend > rbeg ? (int)((rend - rbeg + kR - 1) / kR) : 0;
+
+  if (tid == 0) {
+    for (int q = 0; q < C::NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 4) {  // producer
+    for (int it = 0; it < ntiles; ++it) {
+      const int s = it % C::NS;
+      if (it >= C::NS) mbar_wait(&empty[s], (uint32_t)(((it / C::NS) - 1) & 1));
+      const int64_t r0 = rbeg + (int64_t)it * kR;
+      const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+      issue_tile_load<TW, NP>(Y, cp, r0, nv, stages + s * C::STAGE, &full[s], lane);
+    }
+    return;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  const int plane = CPLX ? (warp >> 1) : 0;
+  const int ks0 = CPLX ? (warp & 1) : warp;
+  double acc[NTILE][2];
+#pragma unroll
+  for (int q = 0; q < NTILE; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % C::NS;
+    mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
+    const double* st = stages + s * C::STAGE;
+    const int64_t r0 = rbeg + (int64_t)it * kR;
+    const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+#pragma unroll
+    for (int ks = ks0; ks < kR / 4; ks += C::KSTRIDE) {
+      const int k = ks * 4 + t;
+      const bool ok = k < nv;
+      double fr[NT], fi[NT];
+#pragma unroll
+      for (int cg = 0; cg < NT; ++cg) {
+        fr[cg] = ok ? st[(size_t)(cg * 8 + g) * kRS + k] : 0.0;
+        fi[cg] = (CPLX && ok) ? st[(size_t)(TW + cg * 8 + g) * kRS + k] : 0.0;
+      }
+      int q = 0;
+#pragma unroll
+      for (int I = 0; I < NT; ++I)
+#pragma unroll
+        for (int J = I; J < NT; ++J, ++q) {
+          if (!CPLX) {
+            dmma884(acc[q][0], acc[q][1], fr[I], fr[J]);
+          } else if (plane == 0) {
+            dmma884(acc[q][0], acc[q][1], fr[I], fr[J]);
+            dmma884(acc[q][0], acc[q][1], fi[I], fi[J]);
+          } else {
+            dmma884(acc[q][0], acc[q][1], fr[I], fi[J]);
+            dmma884(acc[q][0], acc[q][1], -fi[I], fr[J]);
+          }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  consumer_bar();  // every stage consumed: reuse the buffer for the fold
+  double* red = stages;
+#pragma unroll
+  for (int q = 0; q < NTILE; ++q) {
+    red[((size_t)warp * NTILE + q) * 64 + lane * 2] = acc[q][0];
+    red[((size_t)warp * NTILE + q) * 64 + lane * 2 + 1] = acc[q][1];
+  }
+  consumer_bar();
+  double* out = P.gw.part + (((int64_t)pair * 2 + mat) * P.gw.smax + split) * NP * TW * TW;
+  for (int e = tid; e < NP * NTILE * 64; e += 128) {
+    const int pl = e / (NTILE * 64), rem = e % (NTILE * 64), q = rem / 64, l = (rem % 64) / 2, h = rem % 2;
+    double v = 0.0;
+#pragma unroll
+    for (int wv = 0; wv < C::KSTRIDE; ++wv) v += red[((size_t)(pl * C::KSTRIDE + wv) * NTILE + q) * 64 + l * 2 + h];
+    int I = 0, qq = q;
+    while (qq >= NT - I) {
+      qq -= NT - I;
+      ++I;
+    }
+    const int J = I + qq;
+    const int r = I * 8 + (l >> 2), c = J * 8 + 2 * (l & 3) + h;
+    out[(size_t)pl * TW * TW + (size_t)c * TW + r] = v;
+  }
+}
+
+template <int TW, bool CPLX>
+struct PostWsCfg {
+  static constexpr int NP = CPLX ? 2 : 1;
+  static constexpr int TN = TW / 8;  // 8-column tiles, all in one warp
+  static constexpr int NS = CPLX ? 2 : 3;
+  static constexpr int ZS = TW + 4;
+  static constexpr size_t STAGE = (size_t)NP * TW * kRS;
+  static constexpr size_t SMEM = (NS * STAGE + (size_t)NP * TW * ZS) * sizeof(double) + 2 * NS * 8 + 64;
+};
+
+template <int TW, bool CPLX>
+__global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
+  using C = PostWsCfg<TW, CPLX>;
+  constexpr int NP = C::NP;
+  constexpr int w = TW / 2;
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y;
+  if (P.io.ident[pair]) return;
+  const Plane& Y = P.Y[mat];
+  const int64_t rbeg = (int64_t)blockIdx.z * P.chunk;
+  if (rbeg >= Y.rows) return;
+  const int64_t rend = rbeg + P.chunk < Y.rows ? rbeg + P.chunk : Y.rows;
+  const int ntiles = (int)((rend - rbeg + kR - 1) / kR);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stages = reinterpret_cast<double*>(smem_raw);
+  double* zs = stages + C::NS * C::STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(zs + (size_t)NP * TW * C::ZS);
+  uint64_t* done = full + C::NS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
+
+  if (tid == 0) {
+    for (int q = 0; q < C::NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&done[q], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == 4) {  // producer: loads, and stores of finished tiles
+    auto store_tile = [&](int it) {
+      const int s = it % C::NS;
+      mbar_wait(&done[s], (uint32_t)((it / C::NS) & 1));
+      const int64_t r0 = rbeg + (int64_t)it * kR;
+      const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+      const uint32_t bytes = (uint32_t)nv * 8u;
+      const double* st = stages + s * C::STAGE;
+      for (int q = lane; q < TW * NP; q += 32) {
+        const int c = q % TW, pl = q / TW;
+        double* base = pl == 0 ? Y.re : Y.im;
+        bulk_s2g(base + pair_col(cp, w, c) * Y.ld + r0, st + (size_t)q * kRS, bytes);
+      }
+      bulk_commit();
+    };
+    for (int it = 0; it < ntiles; ++it) {
+      const int s = it % C::NS;
+      if (it >= C::NS) {
+        store_tile(it - C::NS);
+        bulk_wait_read<0>();
+        __syncwarp();
+      }
+      const int64_t r0 = rbeg + (int64_t)it * kR;
+      const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+      issue_tile_load<TW, NP>(Y, cp, r0, nv, stages + s * C::STAGE, &full[s], lane);
+    }
+    for (int it = ntiles > C::NS ? ntiles - C::NS : 0; it < ntiles; ++it) store_tile(it);
+    bulk_wait_all<0>();
+    return;
+  }
+  // consumers: Z~ into padded shared memory (column-major)
+  const double* zsrc = P.io.zt + (int64_t)pair * NP * TW * TW;
+  for (int e = tid; e < NP * TW * TW; e += 128) {
+    int p = e / (TW * TW), r = e % TW, c = (e / TW) % TW;
+    zs[(size_t)p * TW * C::ZS + (size_t)c * C::ZS + r] = zsrc[e];
+  }
+  consumer_bar();
+  const int g = lane >> 2, t = lane & 3;
+  for (int it = 0; it < ntiles; ++it) {
+    const int s = it % C::NS;
+    mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
+    double* st = stages + s * C::STAGE;
+    double acc[NP][2][C::TN][2];
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < C::TN; ++ni) acc[p][mi][ni][0] = acc[p][mi][ni][1] = 0.0;
+#pragma unroll 2
+    for (int ks = 0; ks < TW / 4; ++ks) {
+      const int k = ks * 4 + t;
+      double ar[2], ai[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int row = warp * 16 + mi * 8 + g;
+        ar[mi] = st[(size_t)k * kRS + row];
+        ai[mi] = CPLX ? st[(size_t)(TW + k) * kRS + row] : 0.0;
+      }
+#pragma unroll
+      for (int ni = 0; ni < C::TN; ++ni) {
+        const int col = ni * 8 + g;
+        const double zr = zs[(size_t)col * C::ZS + k];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) dmma884(acc[0][mi][ni][0], acc[0][mi][ni][1], ar[mi], zr);
+        if (CPLX) {
+          const double zi = zs[(size_t)TW * C::ZS + (size_t)col * C::ZS + k];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            dmma884(acc[0][mi][ni][0], acc[0][mi][ni][1], -ai[mi], zi);
+            dmma884(acc[NP - 1][mi][ni][0], acc[NP - 1][mi][ni][1], ar[mi], zi);
+            dmma884(acc[NP - 1][mi][ni][0], acc[NP - 1][mi][ni][1], ai[mi], zr);
+          }
+        }
+      }
+    }
+    __syncwarp();  // this warp owns its 16 rows: write them back in place
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < C::TN; ++ni) {
+          const int row = warp * 16 + mi * 8 + g;
+          const int col = ni * 8 + 2 * t;
+          st[(size_t)(p * TW + col) * kRS + row] = acc[p][mi][ni][0];
+          st[(size_t)(p * TW + col + 1) * kRS + row] = acc[p][mi][ni][1];
+        }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[s]);
+  }
+}
+
 template <typename K>
 void set_smem(K k, size_t bytes) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -350,6 +731,45 @@ int gram_t(const GramParams& p, cudaStream_t s) {
   }
   dim3 grid(p.sp.pn, 2, p.gw.smax);
   k_gram_dmma<TW, CPLX><<<grid, C::NWARP * 32, C::SMEM, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <int TW, bool CPLX>
+int gram_ks_t(const GramParams& p, cudaStream_t s) {
+  using C = GramKsCfg<TW, CPLX>;
+  static bool once = false;
+  if (!once) {
+    set_smem(k_gram_ks<TW, CPLX>, C::SMEM);
+    once = true;
+  }
+  dim3 grid(p.sp.pn, 2, p.gw.smax);
+  k_gram_ks<TW, CPLX><<<grid, 128, C::SMEM, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <int TW, bool CPLX>
+int gram_ws_t(const GramParams& p, cudaStream_t s) {
+  using C = GramWsCfg<TW, CPLX>;
+  static bool once = false;
+  if (!once) {
+    set_smem(k_gram_ws<TW, CPLX>, C::SMEM);
+    once = true;
+  }
+  dim3 grid(p.sp.pn, 2, p.gw.smax);
+  k_gram_ws<TW, CPLX><<<grid, 160, C::SMEM, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+template <int TW, bool CPLX>
+int post_ws_t(const PostParams& p, int64_t mmax, cudaStream_t s) {
+  using C = PostWsCfg<TW, CPLX>;
+  static bool once = false;
+  if (!once) {
+    set_smem(k_post_ws<TW, CPLX>, C::SMEM);
+    once = true;
+  }
+  dim3 grid(p.sp.pn, 3, (unsigned)((mmax + p.chunk - 1) / p.chunk));
+  k_post_ws<TW, CPLX><<<grid, 160, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -375,9 +795,9 @@ int launch_gram_dmma(const Plane& F, const Plane& G, const StepPairs& sp, int st
   GramParams p{{F, G}, sp, step, gw};
   switch (2 * w) {
     case 16:
-      return cplx ? gram_t<16, true>(p, s) : gram_t<16, false>(p, s);
+      return cplx ? gram_ws_t<16, true>(p, s) : gram_ws_t<16, false>(p, s);
     case 32:
-      return cplx ? gram_t<32, true>(p, s) : gram_t<32, false>(p, s);
+      return cplx ? gram_ws_t<32, true>(p, s) : gram_ws_t<32, false>(p, s);
     case 64:
       return cplx ? gram_t<64, true>(p, s) : gram_t<64, false>(p, s);
   }
@@ -388,13 +808,14 @@ int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const S
                          int cplx, const InnerOut& io, cudaStream_t s) {
   int64_t mmax = F.rows > G.rows ? F.rows : G.rows;
   if (Z.rows > mmax) mmax = Z.rows;
-  PostParams p{{F, G, Z}, sp, step, io, 512};
+  PostParams p{{F, G, Z}, sp, step, io, 1024};
   switch (2 * w) {
     case 16:
-      return cplx ? post_t<16, true>(p, mmax, s) : post_t<16, false>(p, mmax, s);
+      return cplx ? post_ws_t<16, true>(p, mmax, s) : post_ws_t<16, false>(p, mmax, s);
     case 32:
-      return cplx ? post_t<32, true>(p, mmax, s) : post_t<32, false>(p, mmax, s);
+      return cplx ? post_ws_t<32, true>(p, mmax, s) : post_ws_t<32, false>(p, mmax, s);
     case 64:
+      p.chunk = 512;
       return cplx ? post_t<64, true>(p, mmax, s) : post_t<64, false>(p, mmax, s);
   }
   return 4;
