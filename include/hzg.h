@@ -83,6 +83,15 @@ int hzg_sweep(hzg_ctx* ctx, int64_t* total, int64_t* big);
  * bookkeeping (asynchronous; for profiling and bounded benchmarks). */
 int hzg_run_steps(hzg_ctx* ctx, int32_t first, int32_t count);
 
+/* Step-wise driving for multi-GPU jobs (one rank's slot range of the
+ * ordering per GPU, blocks exchanged between steps by the caller):
+ * hzg_collect folds the per-pair counters of all steps of the schedule
+ * (i.e. of the sweep just run with hzg_run_steps) and returns them
+ * (synchronous); hzg_rescale_z runs the inter-sweep Z rescale of
+ * blocked.py:540-542 on every column (asynchronous). */
+int hzg_collect(hzg_ctx* ctx, int64_t* total, int64_t* big);
+int hzg_rescale_z(hzg_ctx* ctx);
+
 /* Final rescale, unborder to n0 columns (mF0 / mG0 rows) and stable
  * descending sort by sigma (sort = 0 keeps the column order, as
  * gsvd_blocked does), into caller-provided device outputs: U (mF0 x

@@ -24,7 +24,7 @@ class HzgConfig(ctypes.Structure):
 
 
 EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_init_fgz", "hzg_sweep",
-           "hzg_run_steps", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
+           "hzg_run_steps", "hzg_collect", "hzg_rescale_z", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
            "hzg_step_counters", "hzg_debug_phases", "hzg_test_fastmath", "hzg_last_error",
            "hzg_destroy")
 
@@ -57,6 +57,10 @@ def load(path=LIB_PATH):
         L.hzg_sweep.restype = ctypes.c_int
         L.hzg_run_steps.argtypes = [P, I32, I32]
         L.hzg_run_steps.restype = ctypes.c_int
+        L.hzg_collect.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.hzg_collect.restype = ctypes.c_int
+        L.hzg_rescale_z.argtypes = [P]
+        L.hzg_rescale_z.restype = ctypes.c_int
         L.hzg_finalize.argtypes = [P, I64, I64, I64, I32] + [P] * 9
         L.hzg_finalize.restype = ctypes.c_int
         L.hzg_test_block.argtypes = [I32, I32, ctypes.POINTER(HzgConfig), D] + [P] * 6 + [P]

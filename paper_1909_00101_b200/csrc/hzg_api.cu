@@ -512,6 +512,34 @@ int hzg_run_steps(hzg_ctx* c, int32_t first, int32_t count) {
   return HZG_OK;
 }
 
+int hzg_collect(hzg_ctx* c, int64_t* total, int64_t* big) {
+  if (!c || !c->bound) return HZG_INVALID;
+  cudaError_t e;
+  int rc = launch_counters(c->io.counts, (int64_t)c->osteps * c->npairs, c->d_ctr, c->stream);
+  if (rc) return fail(c, rc, "counter fold launch");
+  if ((e = cudaMemcpyAsync(c->h_ctr, c->d_ctr, 3 * 8, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "counter copy");
+  if ((e = cudaMemcpyAsync(c->h_ctr + 3, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "status copy");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "collect");
+  if (total) *total = c->h_ctr[0];
+  if (big) *big = c->h_ctr[1];
+  rc = status_code(c->h_ctr[2]);
+  if (rc == HZG_NOT_PD) return fail(c, rc, "indefinite block Grammian; enable the QR fallback");
+  if (rc == HZG_RANK) return fail(c, rc, "rank-deficient block pair in the inner solve");
+  int32_t st = 0;
+  std::memcpy(&st, c->h_ctr + 3, 4);
+  if (st) return fail(c, HZG_RANK, "zero pencil column between sweeps");
+  return HZG_OK;
+}
+
+int hzg_rescale_z(hzg_ctx* c) {
+  if (!c || !c->bound) return HZG_INVALID;
+  int rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 0, nullptr, nullptr, nullptr, nullptr, c->d_status,
+                          c->stream);
+  return rc ? fail(c, rc, "rescale launch") : HZG_OK;
+}
+
 int hzg_finalize(hzg_ctx* c, int64_t n0, int64_t mF0, int64_t mG0, int32_t sort, double* Ur, double* Ui, double* Vr,
                  double* Vi, double* Zr, double* Zi, double* sigF, double* sigG, double* sig) {
   if (!c || !c->bound || n0 < 1 || n0 > c->n || mF0 > c->mF || mG0 > c->mG) return HZG_INVALID;

@@ -1,0 +1,223 @@
+"""Block-partitioned multi-GPU GSVD (the paper's multi-GPU algorithm, PAPER.md
+§4, re-designed for one NVSwitch node).
+
+Every outer step keeps the reference's ME pair sets (strategies.py:59-70).
+Pairs are placed by their circle-method position; rank r owns a contiguous
+range of positions.  Between two steps every block moves by one position,
+so only the blocks at the ends of each range change owner: at most two
+blocks leave and two arrive per rank and step, exchanged with NCCL
+send/recv over NVLink (grouped, device to device).
+
+Each rank keeps full-size F, G, Z planes; a block always lives at its
+logical column offset (block b = columns [b w, (b+1) w)), so a block
+exchange is a contiguous copy of w columns of each plane and the kernels
+take the rank's slice of the schedule unchanged.  Per-pair work is
+identical to the single-GPU path (same kernels, same Grammian split
+geometry, same per-pair data), so the result is bitwise independent of the
+number of ranks; the per-sweep counters are integers summed with an
+all-reduce.
+
+Transports:
+  * DistTransport -- torch.distributed P2P (NCCL on GPUs; gloo for the CPU
+    tests of the routing);
+  * LocalTransport -- R virtual ranks in one process (one device), block
+    exchange by device copies; used by solve(workers=R) and the tests.
+"""
+
+import math
+
+import numpy as np
+
+from .strategies import circle_positions, slot_ranges
+
+
+class BlockSchedule:
+    """Circle-position schedule of nblk blocks over nranks ranks."""
+
+    def __init__(self, nblk, nranks):
+        if nblk < 2 or nblk % 2:
+            raise ValueError("need an even number of blocks")
+        if nranks < 1 or nranks > nblk // 2:
+            raise ValueError("need 1 <= ranks <= blocks / 2 (got %d ranks, %d blocks)" % (nranks, nblk))
+        self.nblk = nblk
+        self.nranks = nranks
+        self.steps = nblk - 1
+        self.pos = circle_positions(nblk)            # (steps, nblk/2, 2), (min, max)
+        self.ranges = slot_ranges(nblk // 2, nranks)
+        owner = np.empty((self.steps, nblk), dtype=np.int64)
+        for r, (lo, hi) in enumerate(self.ranges):
+            for k in range(self.steps):
+                owner[k, self.pos[k, lo:hi, 0]] = r
+                owner[k, self.pos[k, lo:hi, 1]] = r
+        self.owner = owner
+
+    def colpairs(self, rank, w):
+        """int32 (steps, npairs_rank, 2): column offsets of the rank's pairs."""
+        lo, hi = self.ranges[rank]
+        return np.ascontiguousarray(self.pos[:, lo:hi, :] * w, dtype=np.int32)
+
+    def moves(self, k):
+        """Blocks changing owner between step k and step (k+1) mod steps:
+        sorted list of (block, src_rank, dst_rank)."""
+        a = self.owner[k]
+        b = self.owner[(k + 1) % self.steps]
+        return [(int(blk), int(a[blk]), int(b[blk])) for blk in np.nonzero(a != b)[0]]
+
+    def owned(self, k, rank):
+        return np.nonzero(self.owner[k] == rank)[0]
+
+
+def _block_views(planes, b, w):
+    """Contiguous (w, m) views of block b of every plane (column-major planes
+    are stored as (cols, rows) tensors, so w consecutive columns are one
+    contiguous chunk)."""
+    out = []
+    for key in ("Fr", "Fi", "Gr", "Gi", "Zr", "Zi"):
+        t = planes.get(key)
+        if t is not None:
+            out.append(t[b * w:(b + 1) * w])
+    return out
+
+
+class LocalTransport:
+    """R virtual ranks in one process: planes_by_rank[r] are that rank's planes."""
+
+    def __init__(self, planes_by_rank, w):
+        self.planes = planes_by_rank
+        self.w = w
+
+    def exchange(self, moves):
+        for (b, src, dst) in moves:
+            for s, d in zip(_block_views(self.planes[src], b, self.w), _block_views(self.planes[dst], b, self.w)):
+                d.copy_(s)
+
+
+class DistTransport:
+    """torch.distributed point-to-point (NCCL between GPUs, gloo on CPU)."""
+
+    def __init__(self, planes, w, rank, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.planes = planes
+        self.w = w
+        self.rank = rank
+        self.group = group
+
+    def exchange(self, moves):
+        dist = self.dist
+        ops = []
+        for (b, src, dst) in moves:
+            if src == self.rank:
+                for t in _block_views(self.planes, b, self.w):
+                    ops.append(dist.P2POp(dist.isend, t, dst, self.group))
+            elif dst == self.rank:
+                for t in _block_views(self.planes, b, self.w):
+                    ops.append(dist.P2POp(dist.irecv, t, src, self.group))
+        if ops:
+            for wk in dist.batch_isend_irecv(ops):
+                wk.wait()
+
+
+def gather_blocks(sched, k_final=0):
+    """(block, owner, 0) moves bringing every block to rank 0 at step k_final."""
+    return [(b, int(sched.owner[k_final, b]), 0) for b in range(sched.nblk) if sched.owner[k_final, b] != 0]
+
+
+def run_ranks(devs, sched, transport, cfg, allreduce=None, rescale_all=None):
+    """The outer sweep loop (blocked.py:503-550) for block-partitioned ranks.
+
+    devs: the DeviceGsvd objects this process drives (all R virtual ranks,
+    or the single local rank).  allreduce(total, big) -> (total, big) sums
+    the counters over processes (identity for virtual ranks).
+    Returns (sweeps, total, big, converged)."""
+    for d in devs:
+        d.init()
+    sweeps = total = big = 0
+    converged = False
+    for _ in range(cfg.max_outer_sweeps):
+        for k in range(sched.steps):
+            for d in devs:
+                d.run_steps(k, 1)
+            transport.exchange(sched.moves(k))
+        t = b = 0
+        for d in devs:
+            tt, bb = d.collect()
+            t += tt
+            b += bb
+        if allreduce is not None:
+            t, b = allreduce(t, b)
+        sweeps += 1
+        total += t
+        big += b
+        if b == 0:
+            converged = True
+            break
+        for d in devs:
+            d.rescale_z()
+    return sweeps, total, big, converged
+
+
+def epsn_of(cfg, n):
+    return cfg.gate_eps * math.sqrt(n)
+
+
+def solve_blocks(F, G, cfg, nranks, comm=None):
+    """GSVD of (F, G) with the block-partitioned schedule over nranks ranks.
+
+    comm=None: nranks virtual ranks in this process on the current device
+    (block exchange by device copies).  comm="dist": this process is one
+    rank of an initialized torch.distributed job (NCCL, one GPU per rank);
+    every rank passes the same F, G and rank 0 returns the result (the
+    others return None).  Results are bitwise those of nranks = 1.
+    """
+    import torch
+
+    from .config import SolverConfig
+    from .core import MatrixPlanePair, ProblemPair
+    from .solver import DeviceGsvd, _result_from_device, gsvd_1x1, upload_bordered
+
+    cfg = cfg or SolverConfig()
+    if isinstance(F, np.ndarray):
+        F = MatrixPlanePair.from_dense(F)
+    if isinstance(G, np.ndarray):
+        G = MatrixPlanePair.from_dense(G)
+    if F.cols == 1:
+        return gsvd_1x1(F, G)
+    p = ProblemPair(F, G)
+    w = cfg.block_width
+    planes0, n, mF, mG = upload_bordered(p.F, p.G, w)
+    nblk = n // w
+    nranks_eff = max(1, min(nranks, nblk // 2))
+    sched = BlockSchedule(nblk, nranks_eff)
+    epsn = epsn_of(cfg, n)
+    if comm is None:
+        plist = [planes0] + [{k: (v.clone() if v is not None else None) for k, v in planes0.items()}
+                             for _ in range(nranks_eff - 1)]
+        devs = [DeviceGsvd(plist[r], cfg, epsn=epsn, schedule=sched.colpairs(r, w)) for r in range(nranks_eff)]
+        tr = LocalTransport([dict(pl, Zr=d.Zr, Zi=d.Zi) for pl, d in zip(plist, devs)], w)
+        sweeps, total, big, conv = run_ranks(devs, sched, tr, cfg)
+        tr.exchange(gather_blocks(sched))
+        root = devs[0]
+    else:
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        if world != nranks_eff:
+            raise ValueError("distributed solve needs world size %d for %d blocks" % (nranks_eff, nblk))
+        dev = DeviceGsvd(planes0, cfg, epsn=epsn, schedule=sched.colpairs(rank, w))
+        tr = DistTransport(dict(planes0, Zr=dev.Zr, Zi=dev.Zi), w, rank)
+
+        def allreduce(t, b):
+            x = torch.tensor([t, b], dtype=torch.int64, device=dev.device)
+            dist.all_reduce(x)
+            return int(x[0]), int(x[1])
+
+        sweeps, total, big, conv = run_ranks([dev], sched, tr, cfg, allreduce)
+        tr.exchange(gather_blocks(sched))
+        if rank != 0:
+            dev.close()
+            return None
+        root = dev
+    root.sweeps, root.total, root.big, root.converged = sweeps, total, big, conv
+    out = root.finalize(p.n, p.F.rows, p.G.rows, sort=True)
+    r = _result_from_device(root, out, p.is_complex, workers=nranks_eff)
+    return r

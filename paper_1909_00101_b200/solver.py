@@ -127,6 +127,17 @@ class DeviceGsvd:
                 break
         return self
 
+    def collect(self):
+        """Fold the per-pair counters of the schedule's steps (one sweep run
+        step by step): (total, big)."""
+        tot = ctypes.c_int64(0)
+        big = ctypes.c_int64(0)
+        _native.check(self.lib.hzg_collect(self.ctx, ctypes.byref(tot), ctypes.byref(big)), self.ctx, "collect")
+        return tot.value, big.value
+
+    def rescale_z(self):
+        _native.check(self.lib.hzg_rescale_z(self.ctx), self.ctx, "rescale_z")
+
     def step_counters(self):
         """int32 (osteps, npairs, 4): total, big, status, inner sweeps of the last sweep."""
         cnt = ctypes.c_int64(0)
@@ -248,10 +259,13 @@ def gsvd_blocked(p, cfg=None, epsn=None):
 def solve(F, G, cfg=None, workers=1, worker_sweeps=1):
     """Border, solve on the GPU, unborder, and sort a GSVD problem.
 
-    F and G may be MatrixPlanePair values or numpy arrays.  ``workers``
-    records the number of cooperating GPUs; results do not depend on it
-    (the block schedule is GPU-count invariant, see strategies.py), so a
-    single-process call runs the whole schedule on the current device.
+    F and G may be MatrixPlanePair values or numpy arrays.  With
+    ``workers`` > 1 the block-partitioned multi-rank schedule (dist.py)
+    runs with that many virtual ranks on the current device; a torchrun job
+    uses dist.solve_blocks(..., comm="dist") with one GPU per rank.  The
+    result does not depend on the rank count.  ``worker_sweeps`` is
+    accepted for signature compatibility (the block schedule has no inner
+    per-worker sweep cap).
     """
     cfg = cfg or SolverConfig()
     if isinstance(F, np.ndarray):
@@ -262,6 +276,9 @@ def solve(F, G, cfg=None, workers=1, worker_sweeps=1):
         raise ValueError("need at least one worker")
     if F.cols == 1:
         return gsvd_1x1(F, G)
+    if workers > 1:
+        from .dist import solve_blocks
+        return solve_blocks(F, G, cfg, workers)
     p = ProblemPair(F, G)
     planes, n, mF, mG = upload_bordered(p.F, p.G, cfg.block_width)
     dev = DeviceGsvd(planes, cfg)

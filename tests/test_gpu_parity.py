@@ -242,3 +242,35 @@ def test_qr_fallback_dmma_residuals():
         m = gsvd_metrics(c["F"], c["G"], r)
         assert m["resF"] <= 1e-12 and m["resG"] <= 1e-12, (name, m)
         assert m["orthU"] <= 1e-12 and m["orthV"] <= 1e-12, (name, m)
+
+
+# ---------------------------------------------------------------------------
+# multi-rank block schedule (virtual ranks on one device): bitwise invariant
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name,exact", [("genpair256_w16", False), ("corpus64_complex_w8", False),
+                                        ("corpus64_real_w8", True), ("complex_tall48x32_w4", True)])
+def test_block_partitioned_ranks_bitwise_equal_single(name, exact):
+    c = load_case(name)
+    cfg = _cfg(c, exact=exact)
+    one = hz.solve(c["F"], c["G"], cfg)
+    for ranks in (2, 3, 4):
+        r = hz.solve(c["F"], c["G"], cfg, workers=ranks)
+        assert r.workers <= ranks
+        assert (r.sweeps, r.total_transforms, r.big_transforms) == (one.sweeps, one.total_transforms,
+                                                                    one.big_transforms)
+        for a, b in ((r.sigma, one.sigma), (r.U.re, one.U.re), (r.V.re, one.V.re), (r.Z.re, one.Z.re)):
+            assert np.array_equal(a, b)
+        if one.Z.is_complex:
+            assert np.array_equal(r.Z.im, one.Z.im)
+
+
+def test_block_partitioned_1024_eight_ranks():
+    g = O.gaussian_stream(77, 2 * 1024 * 1024)
+    F = g[: 1024 * 1024].reshape((1024, 1024), order="F")
+    G = g[1024 * 1024:].reshape((1024, 1024), order="F")
+    cfg = hz.SolverConfig(block_width=16)
+    one = hz.solve(F, G, cfg)
+    r = hz.solve(F, G, cfg, workers=8)
+    assert r.workers == 8
+    assert np.array_equal(r.sigma, one.sigma) and np.array_equal(r.Z.re, one.Z.re)
