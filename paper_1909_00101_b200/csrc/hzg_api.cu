@@ -58,7 +58,8 @@ struct hzg_ctx {
   bool bound = false;
   // optional per-kernel timing (events captured into the sweep graph)
   bool timing = false;
-  std::vector<cudaEvent_t> tev;  // [osteps][4]
+  std::vector<cudaEvent_t> tev;  // [osteps][groups][4] (sweep graph)
+  std::vector<cudaEvent_t> rev;  // [count][4] (hzg_run_steps)
   double kms[3] = {0, 0, 0};
   int64_t kcnt[3] = {0, 0, 0};
 };
@@ -504,10 +505,33 @@ int hzg_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
 }
 
 int hzg_run_steps(hzg_ctx* c, int32_t first, int32_t count) {
-  if (!c || !c->bound || first < 0 || first + count > c->osteps) return HZG_INVALID;
+  if (!c || !c->bound || first < 0 || count < 0 || first + count > c->osteps) return HZG_INVALID;
+  // with timing on, every kernel is bracketed by events on the launch
+  // stream and the call is synchronous (isolated per-kernel durations)
+  if (c->timing && c->rev.size() < (size_t)count * 4) {
+    size_t old = c->rev.size();
+    c->rev.resize((size_t)count * 4);
+    for (size_t e = old; e < c->rev.size(); ++e) cudaEventCreate(&c->rev[e]);
+  }
   for (int s = first; s < first + count; ++s) {
-    int rc = launch_step(c, s, c->stream);
+    int rc = launch_step(c, s, c->stream, c->timing ? &c->rev[(size_t)(s - first) * 4] : nullptr);
     if (rc) return fail(c, rc, "step launch");
+  }
+  if (c->timing) {
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "run_steps");
+    for (int q = 0; q < count; ++q) {
+      cudaEvent_t* ev = &c->rev[(size_t)q * 4];
+      for (int k = 0; k < 3; ++k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ev[k], ev[k + 1]) == cudaSuccess) {
+          c->kms[k] += ms;
+          c->kcnt[k] += 1;
+        } else {
+          (void)cudaGetLastError();
+        }
+      }
+    }
   }
   return HZG_OK;
 }
@@ -683,6 +707,7 @@ void hzg_destroy(hzg_ctx* c) {
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->h_ctr) cudaFreeHost(c->h_ctr);
   for (auto& e : c->tev) cudaEventDestroy(e);
+  for (auto& e : c->rev) cudaEventDestroy(e);
   for (auto& e : c->gevents) cudaEventDestroy(e);
   for (auto& s : c->gstreams) cudaStreamDestroy(s);
   delete c;

@@ -23,17 +23,32 @@ namespace {
 
 constexpr int kMaxTW = 64;
 
-template <int TW, bool CPLX>
+// Work split of the pointwise sweeps: NW warps, each owning PPW pivots of
+// every inner step (dot products, the 2x2 math in lanes 0..PPW-1, and the
+// column updates), so the only CTA-wide barrier of an inner step is the one
+// that hands the updated columns to the next step's pivots.
+template <int TW, bool CPLX, int PPWM = 0>
+struct InnerGeo {
+  static constexpr int NPIV = TW / 2;                    // pivots per inner step
+  static constexpr int PPWMAX = PPWM > 0 ? PPWM : ((CPLX && TW > 32) ? 2 : 4);
+  static constexpr int NW = (NPIV + PPWMAX - 1) / PPWMAX;
+  static constexpr int PPW = (NPIV + NW - 1) / NW;
+  static constexpr int Q = 8 * PPW;                      // reduced quantities per warp
+  static constexpr int QP = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
+  static constexpr int LQ = QP == 8 ? 3 : (QP == 16 ? 4 : 5);
+};
+
+template <int TW, bool CPLX, int PPWM = 0>
 struct InnerSmem {
+  using Geo = InnerGeo<TW, CPLX, PPWM>;
   static constexpr int NP = CPLX ? 2 : 1;
   double A[NP][TW * TW];  // F-hat, column-major (element (r, c) at c*TW + r)
   double B[NP][TW * TW];  // G-hat
   double Z[NP][TW * TW];  // Z-hat
   uint8_t tab[TW * TW];   // inner table, (steps, TW/2, 2)
-  double pd[TW / 2][9];   // phase A -> B: a11 a22 a12r b11 b22 b12r a12i b12i (stride 9: no bank conflicts)
-  double px[TW / 2][7];   // phase B -> C: z11 z12r z12i z21r z21i z22 (stride 7)
-  int pflag[TW / 2];
-  int stepbad, sw_applied, sw_big;
+  double wz[Geo::NW][Geo::PPW][6];  // 2x2 math -> column updates (per warp): z11 z12r z12i z21r z21i z22
+  int wf[Geo::NW][Geo::PPW];        // pivot flags: 1 applied, 2 big, 4 swap, 8 bad
+  int wcnt[Geo::NW][2];             // per-warp sweep counters (applied, big)
   int chol_fail[2];
 };
 
@@ -50,6 +65,35 @@ __device__ __forceinline__ double lane_tree(const double (&p)[EPL]) {
   if (EPL == 2) v = p[0] + p[1];
   return warp_tree(v);
 }
+
+// Recursive-halving butterfly over CUR quantities per lane: at xor distance
+// 2^J every lane keeps half of its partial sums (chosen by lane bit J) and
+// adds the partner's partials of the same half, until one value per lane
+// is left; remaining levels are plain butterflies.  Every partial stays the
+// sum of two aligned neighbour blocks, so each total is bitwise the
+// reference's pairwise tree (dotprod.py:79-91).  Quantity q ends in every
+// lane whose low LQ bits are q's bits reversed.
+template <int CUR, int J>
+struct HalvingTree {
+  static __device__ __forceinline__ void run(double* v, int lane) {
+    if constexpr (J < 5) {
+      if constexpr (CUR > 1) {
+        constexpr int H = CUR / 2;
+        const bool b = (lane >> J) & 1;
+#pragma unroll
+        for (int q = 0; q < H; ++q) {
+          const double keep = b ? v[q + H] : v[q];
+          const double send = b ? v[q] : v[q + H];
+          v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << J);
+        }
+        HalvingTree<H, J + 1>::run(v, lane);
+      } else {
+        v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1 << J);
+        HalvingTree<1, J + 1>::run(v, lane);
+      }
+    }
+  }
+};
 
 template <int TW, bool CPLX>
 __device__ __forceinline__ void load_col(const double* __restrict__ re, const double* __restrict__ im, int col,
@@ -333,14 +377,16 @@ struct InnerParams {
   int32_t* qr_locks;
 };
 
-template <int TW, bool CPLX, int PPW>
-__global__ void __launch_bounds__(TW / 2 / PPW * 32) k_inner(InnerParams P) {
-  constexpr int NPIV = TW / 2;      // pivots per inner step
-  constexpr int NW = NPIV / PPW;    // warps: each forms / applies PPW pivots
+template <int TW, bool CPLX, int PPWM>
+__global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(InnerParams P) {
+  using Geo = InnerGeo<TW, CPLX, PPWM>;
+  constexpr int NPIV = Geo::NPIV;
+  constexpr int NW = Geo::NW;    // warps
+  constexpr int PPW = Geo::PPW;  // pivots per warp and inner step
   constexpr int EPL = Lanes<TW>::EPL;
   constexpr int NP = CPLX ? 2 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& S = *reinterpret_cast<InnerSmem<TW, CPLX>*>(smem_raw);
+  auto& S = *reinterpret_cast<InnerSmem<TW, CPLX, PPWM>*>(smem_raw);
   const int pair = P.sp.p0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = blockDim.x;
@@ -477,38 +523,54 @@ __global__ void __launch_bounds__(TW / 2 / PPW * 32) k_inner(InnerParams P) {
   if (__syncthreads_or(pbad) && status == ST_OK) status = ST_RANK;
 
   // ---- pointwise sweeps (pointwise.py:222-251) ---------------------------
-  // Three phases per inner step, so the scalar 2x2 math runs once per pivot
-  // instead of once per lane of 32:
-  //   A) warp p forms pivot p's six (eight, complex) column dot products by
-  //      a butterfly tree and parks them in shared memory;
-  //   B) warp 0, lane p, runs _k_process_pivot's scalar logic for pivot p
-  //      (gate, transform, big/sort decisions) and parks Z-hat entries;
-  //   C) warp p applies the 2x2 transform / swap to its columns.
+  // Per inner step, warp w owns pivots w*PPW .. w*PPW+PPW-1:
+  //   A) forms their six (eight, complex) column dot products with one
+  //      recursive-halving tree and gathers pivot k's sums into lane k;
+  //   B) lane k runs _k_process_pivot's scalar logic for pivot k (gate,
+  //      transform, big / sort decisions) and parks the Z-hat entries in the
+  //      warp's slot of shared memory;
+  //   C) the warp applies the transforms / swaps to its pivots' columns.
+  // Pivots of a step touch disjoint columns, so the only CTA barrier is the
+  // one before the next step reads columns other warps wrote.
   int total = 0, big = 0, sweeps = 0;
   if (status == ST_OK) {
     const bool prof = P.io.phase != nullptr && blockIdx.x == 0 && tid == 0;
     long long tA = 0, tB = 0, tC = 0, nstep = 0, c0 = 0, c1 = 0;
     for (int sw = 0; sw < kc.max_inner_sweeps; ++sw) {
-      int lane_applied = 0, lane_big = 0;  // warp 0, lane p: pivot p's counts this sweep
-      for (int st = 0; st < P.isteps; ++st) {
-        if (prof) c0 = clock64();
-        // ---- phase A (pivot pv = warp + k * NW, k < PPW)
-        int ii[PPW], jj[PPW];
-        double fi[PPW][EPL], fii[PPW][EPL], fj[PPW][EPL], fji[PPW][EPL];
-        double gi[PPW][EPL], gii[PPW][EPL], gj[PPW][EPL], gji[PPW][EPL];
+      int lane_applied = 0, lane_big = 0;  // lane k: pivot k's counts this sweep
+      // pivot indices of the warp's pivots, fetched one inner step ahead
+      auto fetch = [&](int st, int (&a)[PPW], int (&b)[PPW]) {
 #pragma unroll
         for (int k = 0; k < PPW; ++k) {
-          const int pv = warp + k * NW;
-          ii[k] = S.tab[(st * NPIV + pv) * 2];
-          jj[k] = S.tab[(st * NPIV + pv) * 2 + 1];
+          const int pv = warp * PPW + k;
+          const bool ok = NPIV % PPW == 0 || pv < NPIV;
+          a[k] = ok ? S.tab[(st * NPIV + pv) * 2] : 0;
+          b[k] = ok ? S.tab[(st * NPIV + pv) * 2 + 1] : 0;
+        }
+      };
+      int nii[PPW], njj[PPW];
+      fetch(0, nii, njj);
+      for (int st = 0; st < P.isteps; ++st) {
+        if (prof) c0 = clock64();
+        // ---- phase A
+        int ii[PPW], jj[PPW];
+#pragma unroll
+        for (int k = 0; k < PPW; ++k) {
+          ii[k] = nii[k];
+          jj[k] = njj[k];
+        }
+        fetch(st + 1 < P.isteps ? st + 1 : 0, nii, njj);
+        double fi[PPW][EPL], fii[PPW][EPL], fj[PPW][EPL], fji[PPW][EPL];
+        double gi[PPW][EPL], gii[PPW][EPL], gj[PPW][EPL], gji[PPW][EPL];
+        double v[Geo::QP];
+#pragma unroll
+        for (int q = Geo::Q; q < Geo::QP; ++q) v[q] = 0.0;
+#pragma unroll
+        for (int k = 0; k < PPW; ++k) {
           load_col<TW, CPLX>(Ar, Ai, ii[k], lane, fi[k], fii[k]);
           load_col<TW, CPLX>(Ar, Ai, jj[k], lane, fj[k], fji[k]);
           load_col<TW, CPLX>(Br, Bi, ii[k], lane, gi[k], gii[k]);
           load_col<TW, CPLX>(Br, Bi, jj[k], lane, gj[k], gji[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < PPW; ++k) {
-          const int pv = warp + k * NW;
           double p[8][EPL];
 #pragma unroll
           for (int e = 0; e < EPL; ++e) {
@@ -528,97 +590,86 @@ __global__ void __launch_bounds__(TW / 2 / PPW * 32) k_inner(InnerParams P) {
               p[7][e] = 0.0;
             }
           }
-          // Recursive-halving butterfly over the 8 quantities: at xor
-          // distance 1, 2, 4 each lane keeps half of the partial sums and
-          // ships the other half, then xor 8, 16 finish one value per lane.
-          // Every partial is still the sum of two aligned neighbour blocks,
-          // so each total is bitwise the reference's pairwise tree.
-          double v[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = EPL == 2 ? p[q][0] + p[q][EPL - 1] : p[q][0];
-          const bool b0 = lane & 1, b1 = (lane >> 1) & 1, b2 = (lane >> 2) & 1;
-          double s4[4], s2[2];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const double keep = b0 ? v[q + 4] : v[q], send = b0 ? v[q] : v[q + 4];
-            s4[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-          }
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const double keep = b1 ? s4[q + 2] : s4[q], send = b1 ? s4[q] : s4[q + 2];
-            s2[q] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-          }
-          double s1 = (b2 ? s2[1] : s2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? s2[0] : s2[1], 4);
-          s1 = s1 + __shfl_xor_sync(0xffffffffu, s1, 8);
-          s1 = s1 + __shfl_xor_sync(0xffffffffu, s1, 16);
-          if (lane < 8) S.pd[pv][4 * b0 + 2 * b1 + b2] = s1;
+          for (int c = 0; c < 8; ++c) v[k * 8 + c] = EPL == 2 ? p[c][0] + p[c][EPL - 1] : p[c][0];
         }
-        __syncthreads();
+        HalvingTree<Geo::QP, 0>::run(v, lane);
+        // lane k < PPW collects pivot k's eight sums
+        double qv[8];
+        {
+          const int kk = lane < PPW ? lane : 0;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int src = (int)(__brev((unsigned)(kk * 8 + c)) >> (32 - Geo::LQ));
+            qv[c] = __shfl_sync(0xffffffffu, v[0], src);
+          }
+        }
         if (prof) {
           c1 = clock64();
           tA += c1 - c0;
           c0 = c1;
         }
         // ---- phase B: _k_process_pivot's scalar part (pointwise.py:165-207)
-        if (warp == 0) {
-          int flags = 0;  // 1 applied, 2 big, 4 swap, 8 bad
-          if (lane < NPIV) {
-            const double* q = S.pd[lane];
-            double z[6];
-            FastMath fm;
-            flags = pivot_scalar<CPLX>(fm, kc, q, z);
-            if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
-              IeeeMath im;
-              flags = pivot_scalar<CPLX>(im, kc, q, z);
-            }
-            if (flags & 1) {
-#pragma unroll
-              for (int c = 0; c < 6; ++c) S.px[lane][c] = z[c];
-              lane_applied += 1;
-              lane_big += (flags >> 1) & 1;
-            }
-            S.pflag[lane] = flags;
+        int bad = 0;
+        if (lane < PPW && (NPIV % PPW == 0 || warp * PPW + lane < NPIV)) {
+          double z[6];
+          FastMath fm;
+          int flags = pivot_scalar<CPLX>(fm, kc, qv, z);
+          if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
+            IeeeMath im;
+            flags = pivot_scalar<CPLX>(im, kc, qv, z);
           }
-          int anybad = __any_sync(0xffffffffu, flags & 8);
-          if (lane == 0) S.stepbad = anybad;
-          if (st == P.isteps - 1) {
-            int sa = lane_applied, sb = lane_big;
+          if (flags & 1) {
 #pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) {
-              sa += __shfl_xor_sync(0xffffffffu, sa, d);
-              sb += __shfl_xor_sync(0xffffffffu, sb, d);
-            }
-            if (lane == 0) {
-              S.sw_applied = sa;
-              S.sw_big = sb;
-            }
+            for (int c = 0; c < 6; ++c) S.wz[warp][lane][c] = z[c];
+            lane_applied += 1;
+            lane_big += (flags >> 1) & 1;
+          }
+          S.wf[warp][lane] = flags;
+          bad = flags & 8;
+        } else if (lane < PPW) {
+          S.wf[warp][lane] = 0;
+        }
+        if (st == P.isteps - 1) {
+          int sa = lane_applied, sb = lane_big;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            sa += __shfl_xor_sync(0xffffffffu, sa, d);
+            sb += __shfl_xor_sync(0xffffffffu, sb, d);
+          }
+          if (lane == 0) {
+            S.wcnt[warp][0] = sa;
+            S.wcnt[warp][1] = sb;
           }
         }
-        __syncthreads();
+        __syncwarp();
         if (prof) {
           c1 = clock64();
           tB += c1 - c0;
           c0 = c1;
         }
-        if (S.stepbad) {
-          status = ST_RANK;
-          break;
-        }
         // ---- phase C: _k_update_cols / swaps (pointwise.py:178-218)
+        // every shared-memory operand of the warp's pivots is loaded up
+        // front (one latency instead of one per pivot)
+        int fl[PPW];
+        double zz[PPW][6];
+        double zi_[PPW][EPL], zii[PPW][EPL], zj_[PPW][EPL], zji[PPW][EPL];
 #pragma unroll
         for (int k = 0; k < PPW; ++k) {
-          const int pv = warp + k * NW;
+          fl[k] = S.wf[warp][k];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) zz[k][c] = S.wz[warp][k][c];
+          load_col<TW, CPLX>(Zr, Zi, ii[k], lane, zi_[k], zii[k]);
+          load_col<TW, CPLX>(Zr, Zi, jj[k], lane, zj_[k], zji[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < PPW; ++k) {
           const int i = ii[k], j = jj[k];
-          const int flags = S.pflag[pv];
+          const int flags = fl[k];
           bool swap = (flags & 4) != 0;
-          double zi_[EPL], zii[EPL], zj_[EPL], zji[EPL];
-          if (flags & 5) {
-            load_col<TW, CPLX>(Zr, Zi, i, lane, zi_, zii);
-            load_col<TW, CPLX>(Zr, Zi, j, lane, zj_, zji);
-          }
           if (flags & 1) {
-            const double z11 = S.px[pv][0], z12r = S.px[pv][1], z12i = S.px[pv][2];
-            const double z21r = S.px[pv][3], z21i = S.px[pv][4], z22 = S.px[pv][5];
+            const double z11 = zz[k][0], z12r = zz[k][1], z12i = zz[k][2];
+            const double z21r = zz[k][3], z21i = zz[k][4], z22 = zz[k][5];
 #define HZG_UPD(yr, yi, yjr_, yji_)                                                         \
   {                                                                                        \
     double yir = yr[e], yjr = yjr_[e];                                                     \
@@ -639,7 +690,7 @@ __global__ void __launch_bounds__(TW / 2 / PPW * 32) k_inner(InnerParams P) {
             for (int e = 0; e < EPL; ++e) {
               HZG_UPD(fi[k], fii[k], fj[k], fji[k]);
               HZG_UPD(gi[k], gii[k], gj[k], gji[k]);
-              HZG_UPD(zi_, zii, zj_, zji);
+              HZG_UPD(zi_[k], zii[k], zj_[k], zji[k]);
             }
 #undef HZG_UPD
             if (kc.sorting && CPLX) {
@@ -659,18 +710,28 @@ __global__ void __launch_bounds__(TW / 2 / PPW * 32) k_inner(InnerParams P) {
             store_col<TW, CPLX>(Ar, Ai, dj, lane, fj[k], fji[k]);
             store_col<TW, CPLX>(Br, Bi, di, lane, gi[k], gii[k]);
             store_col<TW, CPLX>(Br, Bi, dj, lane, gj[k], gji[k]);
-            store_col<TW, CPLX>(Zr, Zi, di, lane, zi_, zii);
-            store_col<TW, CPLX>(Zr, Zi, dj, lane, zj_, zji);
+            store_col<TW, CPLX>(Zr, Zi, di, lane, zi_[k], zii[k]);
+            store_col<TW, CPLX>(Zr, Zi, dj, lane, zj_[k], zji[k]);
           }
         }
-        __syncthreads();
+        // a rank-deficient pivot anywhere ends the solve (RankError upstream)
+        const int anybad = __syncthreads_or(bad);
         if (prof) {
           tC += clock64() - c0;
           ++nstep;
         }
+        if (anybad) {
+          status = ST_RANK;
+          break;
+        }
       }
       if (status != ST_OK) break;
-      const int s_cnt = S.sw_applied, b_cnt = S.sw_big;
+      int s_cnt = 0, b_cnt = 0;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) {
+        s_cnt += S.wcnt[q][0];
+        b_cnt += S.wcnt[q][1];
+      }
       sweeps += 1;
       if (s_cnt == 0) break;
       total += s_cnt;
@@ -736,31 +797,30 @@ __global__ void __launch_bounds__(TW / 2 / PPW * 32) k_inner(InnerParams P) {
   }
 }
 
+template <int TW, bool CPLX, int PPWM>
+int launch_inner_g(const InnerParams& p, cudaStream_t s) {
+  const size_t smem = sizeof(InnerSmem<TW, CPLX, PPWM>);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_inner<TW, CPLX, PPWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_done = true;
+  }
+  k_inner<TW, CPLX, PPWM><<<p.sp.pn, InnerGeo<TW, CPLX, PPWM>::NW * 32, smem, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 template <int TW, bool CPLX>
 int launch_inner_t(const InnerParams& p, cudaStream_t s) {
-  // pivots per warp in the dot / update phases (HZG_PPW overrides, for tuning)
-  constexpr int kPPW = 1;  // measured best at w = 16 (profiles/r01_notes.md)
-  static int ppw = -1;
-  if (ppw < 0) {
-    ppw = kPPW;
-    if (const char* e = std::getenv("HZG_PPW")) ppw = std::atoi(e);
-    if (ppw != 1 && ppw != 2 && ppw != 4) ppw = kPPW;
-    if (TW / 2 < ppw) ppw = 1;
+  if constexpr (TW == 32 && !CPLX) {
+    // pivots per warp (HZG_PPW=2 selects 8 warps x 2 pivots; for tuning)
+    static int ppw = -1;
+    if (ppw < 0) {
+      const char* e = std::getenv("HZG_PPW");
+      ppw = e ? std::atoi(e) : 4;
+    }
+    if (ppw == 2) return launch_inner_g<TW, CPLX, 2>(p, s);
   }
-  size_t smem = sizeof(InnerSmem<TW, CPLX>);
-  auto launch = [&](auto kern, int ppw_) {
-    static bool attr_done = false;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    (void)attr_done;
-    kern<<<p.sp.pn, TW / 2 / ppw_ * 32, smem, s>>>(p);
-  };
-  if (ppw == 4 && TW / 2 >= 4)
-    launch(k_inner<TW, CPLX, (TW / 2 >= 4 ? 4 : 1)>, TW / 2 >= 4 ? 4 : 1);
-  else if (ppw == 2 && TW / 2 >= 2)
-    launch(k_inner<TW, CPLX, (TW / 2 >= 2 ? 2 : 1)>, TW / 2 >= 2 ? 2 : 1);
-  else
-    launch(k_inner<TW, CPLX, 1>, 1);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+  return launch_inner_g<TW, CPLX, 0>(p, s);
 }
 
 }  // namespace
