@@ -11,14 +11,18 @@ outer sweeps to convergence, final rescale, unborder and sort.
             sweeps * P * c * [12 w^2 (mF + mG) + 8 w^2 n],  P = Nb (Nb - 1) / 2.
 * e2e    -- the same through the public drop-in API solve(): numpy inputs in
             pinned host memory copied in, numpy U, V, Z, sigma copied out.
-* roofline -- per-kernel CUDA-event times captured inside the sweep graph
-            over the timed region; algorithmic bytes per launch / avg time.
+* roofline -- the step kernels run alone over sweep 1 of the same pair
+            (one launch per outer step covering every block pair, CUDA
+            events on the launch stream): algorithmic bytes per launch /
+            average duration, against the measured HBM copy bandwidth.
+* n16384  -- config 5 (iid Gaussian 16384^2) timed over its first sweeps.
 * cpu_baseline -- the CPU oracle (C restatement, bitwise the reference) on
             a bounded sample of outer steps, all host threads.
 
 `--impl reference` times the reference CPU path (the oracle port) alone.
-Multi-GPU (torchrun): independent replicas, one problem per rank (weak
-scaling); the time is the max over ranks.
+Multi-GPU (torchrun, N > 1): ONE problem whose column blocks are partitioned
+over the N ranks (strong scaling), blocks exchanged with NCCL send/recv
+every outer step; the time is the max over ranks.
 """
 
 import argparse
@@ -54,6 +58,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--big-n", type=int, default=16384,
+                    help="also time the first --big-sweeps sweeps of config 5 at this n (0: skip)")
+    ap.add_argument("--big-sweeps", type=int, default=2)
     return ap.parse_args()
 
 
@@ -212,6 +219,72 @@ def run_reference(a):
 # the B200 path
 # ---------------------------------------------------------------------------
 
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
+    except Exception:
+        return {}, "fallback 6650 GB/s (B200_PROFILING.md)"
+
+
+FP64_PEAK_TFLOPS = 37.04  # DMMA.8x8x4 loop on this pool's B200 (profiles/r01_fp64_peak.txt)
+
+
+def isolated_kernels(hz, planes, cfg, n, mF, mG, w, steps):
+    """Per-kernel durations with every step kernel alone on the GPU: one
+    launch covers all pairs of a step; CUDA events on the launch stream.
+    Returns (kernel_times, bytes per launch {gram, post})."""
+    dev = hz.DeviceGsvd(planes, cfg)
+    dev.set_timing(True)
+    dev.init()
+    dev.run_steps(0, steps)
+    kt = dev.kernel_times(reset=True)
+    dev.close()
+    npairs = n // w // 2
+    return kt, {"grammian": npairs * 2 * w * 8 * (mF + mG), "postmult": npairs * 2 * w * 8 * 2 * (mF + mG + n)}
+
+
+def sweep_bytes(n, mF, mG, w):
+    nb = n // w
+    P = nb * (nb - 1) // 2
+    return P * (48 * w * (mF + mG) + 32 * w * n)
+
+
+def big_sweeps(hz, torch, device, n, w, sweeps, seed):
+    """Config 5 (iid Gaussian n x n) bounded to its first `sweeps` outer
+    sweeps (the heaviest ones): FP64 GFLOP/s of the algorithmic count."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    F = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
+    G = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
+    cfg = hz.SolverConfig(block_width=w)
+    dev = hz.DeviceGsvd({"Fr": F, "Gr": G, "Fi": None, "Gi": None}, cfg)
+    dev.init()
+    dev.sweep()  # builds the graph; sweep 1 (also timed below from a fresh start)
+    F2 = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
+    G2 = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
+    F.copy_(F2)
+    G.copy_(G2)
+    del F2, G2
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    dev.init()
+    for _ in range(sweeps):
+        dev.sweep()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    fl = sweeps * flops_per_sweep(n, n, n, w)
+    dev.close()
+    return {"workload": "config5: real FP64 iid-Gaussian F,G %dx%d, w=%d, first %d outer sweeps from the "
+                        "prescale (the heaviest sweeps; a full solve needs ~30+)" % (n, n, w, sweeps),
+            "s_per_sweep": ms / 1e3 / sweeps, "gflops": fl / (ms / 1e3) / 1e9,
+            "fp64_frac": fl / (ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+            "hbm_gbs_algorithmic": sweeps * sweep_bytes(n, n, n, w) / (ms / 1e3) / 1e9}
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -222,6 +295,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1909_00101_b200 as hz
+    from paper_1909_00101_b200.dist import PartitionedGsvd
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -230,37 +304,37 @@ def main():
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-    a.seed += rank  # independent replica per rank
 
+    # every rank generates the same pair; N > 1 partitions its column blocks
     Fr0, Gr0, truth = gen_pair(a, torch, device)
     n = a.n
     cap = a.max_sweeps if a.max_sweeps else (100 if a.kind == "cond" else 30)
     cfg = hz.SolverConfig(block_width=a.w, max_outer_sweeps=cap)
     w = a.w
-    padn = (-n) % (2 * w)
-    assert padn == 0, "bench uses n divisible by 2w"
+    assert n % (2 * w) == 0, "bench uses n divisible by 2w"
     mF = mG = n
     Fw = torch.empty_like(Fr0)
     Gw = torch.empty_like(Gr0)
-    dev = hz.DeviceGsvd({"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}, cfg)
-    dev.set_timing(True)
+    planes = {"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}
+    if world > 1:
+        job = PartitionedGsvd(planes, cfg, world, comm="dist")
+    else:
+        job = hz.DeviceGsvd(planes, cfg)
     F_sweep = flops_per_sweep(n, mF, mG, w)
 
     def step():
         Fw.copy_(Fr0)
         Gw.copy_(Gr0)
-        dev.run()
-        out = dev.finalize(n, mF, mG)
-        return out
+        job.run()
+        return job.finalize(n, mF, mG)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    for _ in range(a.warmup):
+    for _ in range(max(3, a.warmup)):
         out = step()
     torch.cuda.synchronize()
-    dev.kernel_times(reset=True)
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -271,7 +345,7 @@ def main():
     sweeps = []
     for _ in range(a.steps):
         out = step()
-        sweeps.append(dev.sweeps)
+        sweeps.append(job.sweeps)
     e1.record()
     torch.cuda.synchronize()
     barrier()
@@ -281,14 +355,13 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    # one problem for the whole job: the flops are counted once
     flops = sum(s * F_sweep for s in sweeps)
-    fl_t = torch.tensor([float(flops)], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(fl_t)
-    value = float(fl_t.item()) / (ms_max / 1e3) / 1e9
-    kt = dev.kernel_times(reset=True)
+    value = flops / (ms_max / 1e3) / 1e9
+    per_sweep_launches, fixed_launches = job.launch_counts()
+    launches = sum(s * per_sweep_launches + fixed_launches for s in sweeps)
 
-    # accuracy of the last solve (self-consistency + truth), cheap on the GPU
+    # accuracy of the last solve (self-consistency + truth), on the GPU
     acc = {}
     if rank == 0:
         Ur, Vr, Zr = out["Ur"], out["Vr"], out["Zr"]
@@ -300,11 +373,12 @@ def main():
         eye = torch.eye(n, dtype=torch.float64, device=device)
         acc["orthU"] = float(torch.linalg.norm(Ur @ Ur.T - eye))
         acc["orthV"] = float(torch.linalg.norm(Vr @ Vr.T - eye))
+        acc["normalization"] = float(torch.max(torch.abs(sF * sF + sG * sG - 1)))
         if truth is not None:
             tr = torch.sort(truth, descending=True).values
             acc["max_rel_sigma_vs_generator"] = float(torch.max(torch.abs(s - tr) / tr))
 
-    # e2e through the public API with pinned host buffers
+    # e2e through the public drop-in API with pinned host buffers
     ke = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 3))
     Fh = torch.empty(Fr0.shape, dtype=torch.float64, pin_memory=True)
     Gh = torch.empty(Gr0.shape, dtype=torch.float64, pin_memory=True)
@@ -312,14 +386,23 @@ def main():
     Gh.copy_(Gr0)
     Fnp = Fh.numpy().T  # Fortran-order (m, n) views of pinned memory
     Gnp = Gh.numpy().T
-    r = hz.solve(Fnp, Gnp, cfg)  # warm
+    if world > 1:
+        from paper_1909_00101_b200.dist import solve_blocks
+
+        def api():
+            return solve_blocks(Fnp, Gnp, cfg, world, comm="dist")
+    else:
+        def api():
+            return hz.solve(Fnp, Gnp, cfg)
+    r = api()  # warm
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e2e_sweeps = []
     for _ in range(ke):
-        r = hz.solve(Fnp, Gnp, cfg)
-        e2e_sweeps.append(r.sweeps)
+        r = api()
+        if r is not None:
+            e2e_sweeps.append(r.sweeps)
     torch.cuda.synchronize()
     barrier()
     te = time.perf_counter() - t0
@@ -327,51 +410,50 @@ def main():
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     te = float(tt.item())
-    fe = torch.tensor([float(sum(s * F_sweep for s in e2e_sweeps))], dtype=torch.float64, device=device)
-    if world > 1:
-        dist.all_reduce(fe)
-    e2e_value = float(fe.item()) / te / 1e9
+    e2e_value = sum(s * F_sweep for s in e2e_sweeps) / te / 1e9 if e2e_sweeps else None
     h2d = (mF + mG) * n * 8
     d2h = (mF + mG + n) * n * 8 + 3 * n * 8
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        barrier()
+        dist.destroy_process_group()
         return
 
-    # roofline of the streaming kernels (algorithmic bytes per launch)
-    npairs = n // w // 2
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-    except Exception:
-        pass
+    # roofline: every step kernel alone on the GPU over sweep 1 of this pair
+    peaks, peak_src = load_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    post_bytes = npairs * 2 * w * 8 * 2 * (mF + mG + n)
-    gram_bytes = npairs * 2 * w * 8 * (mF + mG)
-    post_ms = kt["postmult"][0] / max(1, kt["postmult"][1])
-    gram_ms = kt["grammian"][0] / max(1, kt["grammian"][1])
-    inner_ms = kt["inner"][0] / max(1, kt["inner"][1])
+    Fw.copy_(Fr0)
+    Gw.copy_(Gr0)
+    kt, bpl = isolated_kernels(hz, planes, cfg, n, mF, mG, w, n // w - 1)
+    avg = {k: v[0] / max(1, v[1]) for k, v in kt.items()}
     tot_k = sum(v[0] for v in kt.values())
-    shares = {k: v[0] / tot_k for k, v in kt.items()} if tot_k > 0 else {}
-    post_gbs = post_bytes / (post_ms / 1e3) / 1e9 if post_ms > 0 else None
-    gram_gbs = gram_bytes / (gram_ms / 1e3) / 1e9 if gram_ms > 0 else None
-    roofline = {"kernel": "k_post_dmma (postmultiply of F, G, Z block pairs)", "bound": "hbm",
-                "achieved": post_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": post_gbs / hbm_peak if post_gbs else None, "traffic": None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s",
-                "bytes_per_launch": post_bytes, "avg_launch_ms": post_ms,
-                "grammian": {"achieved": gram_gbs, "frac": gram_gbs / hbm_peak if gram_gbs else None,
-                             "bytes_per_launch": gram_bytes, "avg_launch_ms": gram_ms},
-                "inner_avg_launch_ms": inner_ms, "kernel_time_shares": shares,
-                "fp64": {"achieved_tflops": value / 1e3 / world, "peak_tflops": 37.04,
-                         "peak_source": "profiles/r01_fp64_peak.txt (DMMA microbenchmark on this pool's B200)",
-                         "frac": value / 1e3 / world / 37.04}}
+    post_gbs = bpl["postmult"] / (avg["postmult"] / 1e3) / 1e9
+    gram_gbs = bpl["grammian"] / (avg["grammian"] / 1e3) / 1e9
+    traffic = None
     traffic_file = os.path.join(ROOT, "profiles", "traffic_w%d_n%d.json" % (w, n))
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
-            roofline["traffic"] = json.load(fh).get("postmult_dram_bytes_per_launch")
+            traffic = json.load(fh).get("postmult_dram_bytes_per_launch")
+    step_bytes = sum(s * sweep_bytes(n, mF, mG, w) for s in sweeps)
+    roofline = {"kernel": "k_post_ws (postmultiply of F, G, Z block pairs; the dominant HBM-bound kernel)",
+                "bound": "hbm", "achieved": post_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": post_gbs / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": bpl["postmult"], "avg_launch_ms": avg["postmult"],
+                "measured": "isolated: sweep 1 of this pair, one launch per step covering all %d pairs, "
+                            "CUDA events on the launch stream" % (n // w // 2),
+                "grammian": {"achieved": gram_gbs, "frac": gram_gbs / hbm_peak, "bytes_per_launch": bpl["grammian"],
+                             "avg_launch_ms": avg["grammian"]},
+                "inner": {"avg_launch_ms": avg["inner"], "bound": "latency (dependent FP64 div/sqrt chains + "
+                                                                 "one CTA barrier per inner step)"},
+                "kernel_time_shares_isolated": {k: v[0] / tot_k for k, v in kt.items()} if tot_k else {},
+                "timed_region_hbm_gbs": step_bytes / (ms_max / 1e3) / 1e9,
+                "fp64": {"achieved_tflops": value / 1e3, "peak_tflops": FP64_PEAK_TFLOPS,
+                         "peak_source": "profiles/r01_fp64_peak.txt (DMMA microbenchmark on this pool's B200)",
+                         "frac": value / 1e3 / FP64_PEAK_TFLOPS}}
+
+    extra = None
+    if world == 1 and a.big_n > 0:
+        extra = big_sweeps(hz, torch, device, a.big_n, w, a.big_sweeps, a.seed + 1)
 
     cpu = None
     if not a.no_cpu and world == 1:
@@ -384,21 +466,23 @@ def main():
                          % (s_cpu, n // w - 1),
                "est_full_solve_s": dt / s_cpu * (n // w - 1) * (sum(sweeps) / len(sweeps))}
 
-    launches_per_solve = [1 + s * (3 * (n // w - 1) + 2) + 1 + 4 for s in sweeps]
     line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": max(3, a.warmup), "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated on the GPU)",
             "config": {"workload": workload_name(a), "n": n, "block_width": w, "sweeps": sweeps,
-                       "max_outer_sweeps": cap, "converged": bool(dev.converged),
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "max_outer_sweeps": cap, "converged": bool(job.converged),
+                       "parallelism": ("column blocks partitioned over %d GPUs (NCCL block exchange per step)"
+                                       % world) if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (F+G+Z = %.0f MB > 126 MB)" % (3 * n * n * 8 / 1e6),
                        "wall_s_per_solve": ms_max / a.steps / 1e3},
             "roofline": roofline, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "steps": ke, "wall_s_per_solve": te / ke},
-            "gpu_launches": int(sum(launches_per_solve)), "clocks": clk, "accuracy": acc}
+            "gpu_launches": int(launches), "clocks": clk, "accuracy": acc, "n16384": extra}
     print(json.dumps(line), flush=True)
     if world > 1:
+        barrier()
         dist.destroy_process_group()
 
 

@@ -127,6 +127,10 @@ int hzg_step_counters(hzg_ctx* ctx, int32_t* out, int64_t capacity, int64_t* cou
  * products), B (2x2 transforms), C (column updates), plus the step count. */
 int hzg_debug_phases(hzg_ctx* ctx, int32_t enable, int64_t* out4);
 
+/* Kernel launches of this library per hzg_sweep, and per solve outside the
+ * sweeps (hzg_init_fgz + hzg_finalize). */
+int hzg_launch_counts(const hzg_ctx* ctx, int64_t* per_sweep, int64_t* per_solve_fixed);
+
 /* Self-check of the branch-free FP64 division / square root used by the
  * 2x2 kernels against the IEEE operators on n random operand pairs:
  * counts4 = {divisions checked, mismatches, roots checked, mismatches}. */

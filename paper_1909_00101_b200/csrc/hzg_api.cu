@@ -168,8 +168,10 @@ void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
     chunk = std::max<int64_t>(32, std::min<int64_t>(P, 2048));
     nsplit = (int)std::max<int64_t>(1, P / chunk);
   } else {
-    chunk = 512;
-    nsplit = (int)pow2c((m + chunk - 1) / chunk);
+    // >= 512 rows per split CTA, at most 8 splits (partials stay a few
+    // percent of the Grammian's HBM reads); chunk a multiple of 64 rows
+    nsplit = (int)std::min<int64_t>(8, pow2c((m + 511) / 512));
+    chunk = ((m + nsplit - 1) / nsplit + 63) / 64 * 64;
   }
 }
 
@@ -220,22 +222,33 @@ KernelCfg kernel_cfg(const hzg_ctx* c) {
   return k;
 }
 
+// Event record inside a stream capture (an external event node of the
+// graph) or on a live stream.
+void record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
+
 int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr, int p0 = 0, int pn = -1) {
   StepPairs sp{c->d_colpair, c->npairs, p0, pn < 0 ? c->npairs : pn};
   KernelCfg kc = kernel_cfg(c);
-  if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+  if (ev) record(ev[0], s);
   int rc = c->use_dmma ? launch_gram_dmma(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s)
                        : launch_gram_exact(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s);
   if (rc) return rc;
-  if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+  if (ev) record(ev[1], s);
   rc = launch_inner(c->F, c->G, sp, step, kc, c->gw, c->d_itable, c->isteps, c->io, c->d_qr, c->qr_slots,
                     c->d_qrlock, s);
   if (rc) return rc;
-  if (ev) cudaEventRecordWithFlags(ev[2], s, cudaEventRecordExternal);
+  if (ev) record(ev[2], s);
   rc = c->use_dmma ? launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s)
                    : launch_postmult_exact(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s);
   if (rc) return rc;
-  if (ev) cudaEventRecordWithFlags(ev[3], s, cudaEventRecordExternal);
+  if (ev) record(ev[3], s);
   return HZG_OK;
 }
 
@@ -690,6 +703,16 @@ int hzg_debug_phases(hzg_ctx* c, int32_t enable, int64_t* out4) {
     cudaMemcpyAsync(out4, c->d_phase, 32, cudaMemcpyDeviceToHost, c->stream);
     cudaStreamSynchronize(c->stream);
   }
+  return HZG_OK;
+}
+
+int hzg_launch_counts(const hzg_ctx* c, int64_t* per_sweep, int64_t* per_solve_fixed) {
+  if (!c) return HZG_INVALID;
+  const int G = c->gexec ? c->groups : choose_groups(c);
+  // sweep graph: 3 step kernels per (step, group), counter fold, rescale
+  if (per_sweep) *per_sweep = (int64_t)c->osteps * G * 3 + 2;
+  // k_prescale; final k_rescale, k_keep, k_keep_count, k_rank, k_gather
+  if (per_solve_fixed) *per_solve_fixed = 6;
   return HZG_OK;
 }
 

@@ -52,6 +52,34 @@ struct InnerSmem {
   int chol_fail[2];
 };
 
+// Pairwise tree over NS (a power of two) strided values: the split
+// partials of one Grammian entry, folded in the reference's tree shape.
+template <int NS>
+__device__ __forceinline__ double split_tree(const double* p, int64_t stride) {
+  if constexpr (NS == 1) {
+    return p[0];
+  } else {
+    return split_tree<NS / 2>(p, stride) + split_tree<NS / 2>(p + (NS / 2) * stride, stride);
+  }
+}
+
+__device__ __forceinline__ double fold_splits(const double* p, int64_t stride, int ns) {
+  switch (ns) {
+    case 1: return split_tree<1>(p, stride);
+    case 2: return split_tree<2>(p, stride);
+    case 4: return split_tree<4>(p, stride);
+    case 8: return split_tree<8>(p, stride);
+    case 16: return split_tree<16>(p, stride);
+    case 32: return split_tree<32>(p, stride);
+    default: {
+      PairwiseAcc<16> acc;
+      acc.reset();
+      for (int q = 0; q < ns; ++q) acc.push(p[(int64_t)q * stride]);
+      return acc.result();
+    }
+  }
+}
+
 // Values of one column held by a warp: lane l owns rows l*EPL .. l*EPL+EPL-1.
 template <int TW>
 struct Lanes {
@@ -407,10 +435,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(Inn
       int r = e % TW, c = e / TW;
       if (r > c) continue;
       for (int pl = 0; pl < NP; ++pl) {
-        PairwiseAcc<9> acc;
-        acc.reset();
-        for (int s = 0; s < ns; ++s) acc.push(base[((int64_t)s * NP + pl) * TW * TW + e]);
-        double v = acc.result();
+        const double v = fold_splits(base + (int64_t)pl * TW * TW + e, (int64_t)NP * TW * TW, ns);
         if (pl == 0) {
           M[0][c * TW + r] = v;
           M[0][r * TW + c] = v;

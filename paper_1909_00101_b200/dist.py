@@ -157,6 +157,77 @@ def run_ranks(devs, sched, transport, cfg, allreduce=None, rescale_all=None):
     return sweeps, total, big, converged
 
 
+class PartitionedGsvd:
+    """One rank of a block-partitioned solve over device-resident planes.
+
+    planes: bordered device planes (same content on every rank); comm:
+    None for R virtual ranks on this device (planes are cloned per rank),
+    or "dist" for the torch.distributed rank this process is.  run() is
+    _algorithm1_loop over the partitioned schedule; finalize() gathers the
+    blocks to rank 0 and returns its device outputs (None elsewhere)."""
+
+    def __init__(self, planes, cfg, nranks, comm=None):
+        import torch
+
+        from .solver import DeviceGsvd
+
+        self.cfg = cfg
+        w = cfg.block_width
+        n = planes["Fr"].shape[0]
+        self.nblk = n // w
+        self.nranks = max(1, min(nranks, self.nblk // 2))
+        self.sched = BlockSchedule(self.nblk, self.nranks)
+        epsn = epsn_of(cfg, n)
+        self.comm = comm
+        if comm is None:
+            plist = [planes] + [{k: (v.clone() if v is not None else None) for k, v in planes.items()}
+                                for _ in range(self.nranks - 1)]
+            self.devs = [DeviceGsvd(plist[r], cfg, epsn=epsn, schedule=self.sched.colpairs(r, w))
+                         for r in range(self.nranks)]
+            self.transport = LocalTransport([dict(pl, Zr=d.Zr, Zi=d.Zi) for pl, d in zip(plist, self.devs)], w)
+            self.rank = 0
+            self.allreduce = None
+        else:
+            import torch.distributed as dist
+            self.rank, world = dist.get_rank(), dist.get_world_size()
+            if world != self.nranks:
+                raise ValueError("distributed solve needs world size %d for %d blocks" % (self.nranks, self.nblk))
+            dev = DeviceGsvd(planes, cfg, epsn=epsn, schedule=self.sched.colpairs(self.rank, w))
+            self.devs = [dev]
+            self.transport = DistTransport(dict(planes, Zr=dev.Zr, Zi=dev.Zi), w, self.rank)
+
+            def allreduce(t, b):
+                x = torch.tensor([t, b], dtype=torch.int64, device=dev.device)
+                dist.all_reduce(x)
+                return int(x[0]), int(x[1])
+
+            self.allreduce = allreduce
+        self.sweeps = self.total = self.big = 0
+        self.converged = False
+
+    def run(self):
+        self.sweeps, self.total, self.big, self.converged = run_ranks(self.devs, self.sched, self.transport, self.cfg,
+                                                                      self.allreduce)
+        return self
+
+    def finalize(self, n0=None, mF0=None, mG0=None, sort=True):
+        self.transport.exchange(gather_blocks(self.sched))
+        if self.rank != 0:
+            return None
+        root = self.devs[0]
+        root.sweeps, root.total, root.big, root.converged = self.sweeps, self.total, self.big, self.converged
+        return root.finalize(n0, mF0, mG0, sort=sort)
+
+    def launch_counts(self):
+        # step-wise driving: 3 kernels per step, plus the counter fold and
+        # the Z rescale per sweep, per rank driven by this process
+        return len(self.devs) * (self.sched.steps * 3 + 2), len(self.devs) + 5
+
+    def close(self):
+        for d in self.devs:
+            d.close()
+
+
 def epsn_of(cfg, n):
     return cfg.gate_eps * math.sqrt(n)
 
@@ -170,11 +241,9 @@ def solve_blocks(F, G, cfg, nranks, comm=None):
     every rank passes the same F, G and rank 0 returns the result (the
     others return None).  Results are bitwise those of nranks = 1.
     """
-    import torch
-
     from .config import SolverConfig
     from .core import MatrixPlanePair, ProblemPair
-    from .solver import DeviceGsvd, _result_from_device, gsvd_1x1, upload_bordered
+    from .solver import _result_from_device, gsvd_1x1, upload_bordered
 
     cfg = cfg or SolverConfig()
     if isinstance(F, np.ndarray):
@@ -186,38 +255,13 @@ def solve_blocks(F, G, cfg, nranks, comm=None):
     p = ProblemPair(F, G)
     w = cfg.block_width
     planes0, n, mF, mG = upload_bordered(p.F, p.G, w)
-    nblk = n // w
-    nranks_eff = max(1, min(nranks, nblk // 2))
-    sched = BlockSchedule(nblk, nranks_eff)
-    epsn = epsn_of(cfg, n)
-    if comm is None:
-        plist = [planes0] + [{k: (v.clone() if v is not None else None) for k, v in planes0.items()}
-                             for _ in range(nranks_eff - 1)]
-        devs = [DeviceGsvd(plist[r], cfg, epsn=epsn, schedule=sched.colpairs(r, w)) for r in range(nranks_eff)]
-        tr = LocalTransport([dict(pl, Zr=d.Zr, Zi=d.Zi) for pl, d in zip(plist, devs)], w)
-        sweeps, total, big, conv = run_ranks(devs, sched, tr, cfg)
-        tr.exchange(gather_blocks(sched))
-        root = devs[0]
-    else:
-        import torch.distributed as dist
-        rank, world = dist.get_rank(), dist.get_world_size()
-        if world != nranks_eff:
-            raise ValueError("distributed solve needs world size %d for %d blocks" % (nranks_eff, nblk))
-        dev = DeviceGsvd(planes0, cfg, epsn=epsn, schedule=sched.colpairs(rank, w))
-        tr = DistTransport(dict(planes0, Zr=dev.Zr, Zi=dev.Zi), w, rank)
-
-        def allreduce(t, b):
-            x = torch.tensor([t, b], dtype=torch.int64, device=dev.device)
-            dist.all_reduce(x)
-            return int(x[0]), int(x[1])
-
-        sweeps, total, big, conv = run_ranks([dev], sched, tr, cfg, allreduce)
-        tr.exchange(gather_blocks(sched))
-        if rank != 0:
-            dev.close()
+    job = PartitionedGsvd(planes0, cfg, nranks, comm)
+    try:
+        job.run()
+        out = job.finalize(p.n, p.F.rows, p.G.rows, sort=True)
+        if out is None:
             return None
-        root = dev
-    root.sweeps, root.total, root.big, root.converged = sweeps, total, big, conv
-    out = root.finalize(p.n, p.F.rows, p.G.rows, sort=True)
-    r = _result_from_device(root, out, p.is_complex, workers=nranks_eff)
-    return r
+        root = job.devs[0]
+        return _result_from_device(root, out, p.is_complex, workers=job.nranks)
+    finally:
+        job.close()

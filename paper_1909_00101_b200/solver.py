@@ -147,6 +147,14 @@ class DeviceGsvd:
                                                  ctypes.byref(cnt)), self.ctx, "step_counters")
         return out.reshape(-1, self.n // self.cfg.block_width // 2, 4)
 
+    def launch_counts(self):
+        """(kernel launches per sweep, launches per solve outside the sweeps)."""
+        a = ctypes.c_int64(0)
+        b = ctypes.c_int64(0)
+        _native.check(self.lib.hzg_launch_counts(self.ctx, ctypes.byref(a), ctypes.byref(b)), self.ctx,
+                      "launch_counts")
+        return a.value, b.value
+
     def run_steps(self, first, count):
         _native.check(self.lib.hzg_run_steps(self.ctx, first, count), self.ctx, "run_steps")
 
