@@ -23,32 +23,37 @@ namespace {
 
 constexpr int kMaxTW = 64;
 
-// Work split of the pointwise sweeps: NW warps, each owning PPW pivots of
-// every inner step (dot products, the 2x2 math in lanes 0..PPW-1, and the
-// column updates), so the only CTA-wide barrier of an inner step is the one
-// that hands the updated columns to the next step's pivots.
-template <int TW, bool CPLX, int PPWM = 0>
+// Work split of the pointwise sweeps.  Each pivot of an inner step is
+// owned by a group of LP lanes of one warp; lane l of the group holds rows
+// l*RPL .. l*RPL+RPL-1 of the pivot's columns (RPL = 4 rows, i.e. the first
+// two levels of the reference's pairwise tree happen in registers), so a
+// dot product needs only log2(LP) shuffle levels and a warp serves PG = 32 /
+// LP pivots at once.  Sub-lane 0 of each group runs the 2x2 math.  The only
+// CTA-wide barrier of an inner step hands the updated columns to the next
+// step's pivots.
+template <int TW, bool CPLX>
 struct InnerGeo {
-  static constexpr int NPIV = TW / 2;                    // pivots per inner step
-  static constexpr int PPWMAX = PPWM > 0 ? PPWM : ((CPLX && TW > 32) ? 2 : 4);
-  static constexpr int NW = (NPIV + PPWMAX - 1) / PPWMAX;
-  static constexpr int PPW = (NPIV + NW - 1) / NW;
-  static constexpr int Q = 8 * PPW;                      // reduced quantities per warp
-  static constexpr int QP = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
-  static constexpr int LQ = QP == 8 ? 3 : (QP == 16 ? 4 : 5);
+  static constexpr int NPIV = TW / 2;  // pivots per inner step
+  static constexpr int LT = TW <= 2 ? 2 : (TW <= 4 ? 4 : (TW <= 8 ? 8 : (TW <= 16 ? 16 : (TW <= 32 ? 32 : 64))));
+  static constexpr int RPL = LT >= 4 ? 4 : LT;  // rows per lane
+  static constexpr int LP = LT / RPL;           // lanes per pivot
+  static constexpr int LV = LP == 1 ? 0 : (LP == 2 ? 1 : (LP == 4 ? 2 : (LP == 8 ? 3 : 4)));
+  static constexpr int PG = 32 / LP;            // pivots per warp
+  static constexpr int NW = (NPIV + PG - 1) / PG;
+  static constexpr int HL = LV < 3 ? LV : 3;    // halving levels over the 8 quantities
+  static constexpr int R = 8 >> HL;             // quantities per lane after halving
+  static constexpr bool VEC = TW % 4 == 0 && RPL == 4;  // 16-byte shared loads / stores
 };
 
-template <int TW, bool CPLX, int PPWM = 0>
+template <int TW, bool CPLX>
 struct InnerSmem {
-  using Geo = InnerGeo<TW, CPLX, PPWM>;
+  using Geo = InnerGeo<TW, CPLX>;
   static constexpr int NP = CPLX ? 2 : 1;
-  double A[NP][TW * TW];  // F-hat, column-major (element (r, c) at c*TW + r)
-  double B[NP][TW * TW];  // G-hat
-  double Z[NP][TW * TW];  // Z-hat
-  uint8_t tab[TW * TW];   // inner table, (steps, TW/2, 2)
-  double wz[Geo::NW][Geo::PPW][6];  // 2x2 math -> column updates (per warp): z11 z12r z12i z21r z21i z22
-  int wf[Geo::NW][Geo::PPW];        // pivot flags: 1 applied, 2 big, 4 swap, 8 bad
-  int wcnt[Geo::NW][2];             // per-warp sweep counters (applied, big)
+  alignas(16) double A[NP][TW * TW];  // F-hat, column-major (element (r, c) at c*TW + r)
+  alignas(16) double B[NP][TW * TW];  // G-hat
+  alignas(16) double Z[NP][TW * TW];  // Z-hat
+  uint8_t tab[TW * TW];               // inner table, (steps, TW/2, 2)
+  int wcnt[Geo::NW][2];               // per-warp sweep counters (applied, big)
   int chol_fail[2];
 };
 
@@ -94,34 +99,79 @@ __device__ __forceinline__ double lane_tree(const double (&p)[EPL]) {
   return warp_tree(v);
 }
 
-// Recursive-halving butterfly over CUR quantities per lane: at xor distance
-// 2^J every lane keeps half of its partial sums (chosen by lane bit J) and
-// adds the partner's partials of the same half, until one value per lane
-// is left; remaining levels are plain butterflies.  Every partial stays the
-// sum of two aligned neighbour blocks, so each total is bitwise the
-// reference's pairwise tree (dotprod.py:79-91).  Quantity q ends in every
-// lane whose low LQ bits are q's bits reversed.
-template <int CUR, int J>
+// Recursive-halving butterfly over CUR quantities per lane inside aligned
+// groups of lanes: at xor distance 2^J every lane keeps half of its partial
+// sums (chosen by lane bit J) and adds the partner's partials of the same
+// half.  Every partial stays the sum of two aligned neighbour blocks, so
+// each total is bitwise the reference's pairwise tree (dotprod.py:79-91).
+// After L levels, slot s of lane l holds quantity s + (CUR >> L) * rev_L(l).
+template <int CUR, int J, int L>
 struct HalvingTree {
   static __device__ __forceinline__ void run(double* v, int lane) {
-    if constexpr (J < 5) {
-      if constexpr (CUR > 1) {
-        constexpr int H = CUR / 2;
-        const bool b = (lane >> J) & 1;
+    if constexpr (J < L) {
+      constexpr int H = CUR / 2;
+      const bool b = (lane >> J) & 1;
 #pragma unroll
-        for (int q = 0; q < H; ++q) {
-          const double keep = b ? v[q + H] : v[q];
-          const double send = b ? v[q] : v[q + H];
-          v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << J);
-        }
-        HalvingTree<H, J + 1>::run(v, lane);
-      } else {
-        v[0] = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1 << J);
-        HalvingTree<1, J + 1>::run(v, lane);
+      for (int q = 0; q < H; ++q) {
+        const double keep = b ? v[q + H] : v[q];
+        const double send = b ? v[q] : v[q + H];
+        v[q] = keep + __shfl_xor_sync(0xffffffffu, send, 1 << J);
       }
+      HalvingTree<H, J + 1, L>::run(v, lane);
     }
   }
 };
+
+// Rows r0 .. r0+RPL-1 of column `col` of a TW x TW column-major matrix
+// (zeros beyond TW, like the reference's tree padding).
+template <int TW, bool VEC, int RPL>
+__device__ __forceinline__ void load_rows(const double* m, int col, int r0, double (&x)[RPL]) {
+  if constexpr (VEC) {
+    if (r0 < TW) {
+      const double2* p = reinterpret_cast<const double2*>(m + col * TW + r0);
+#pragma unroll
+      for (int e = 0; e < RPL / 2; ++e) {
+        const double2 d = p[e];
+        x[2 * e] = d.x;
+        x[2 * e + 1] = d.y;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < RPL; ++e) x[e] = 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) x[e] = r0 + e < TW ? m[col * TW + r0 + e] : 0.0;
+  }
+}
+
+template <int TW, bool VEC, int RPL>
+__device__ __forceinline__ void store_rows(double* m, int col, int r0, const double (&x)[RPL]) {
+  if constexpr (VEC) {
+    if (r0 < TW) {
+      double2* p = reinterpret_cast<double2*>(m + col * TW + r0);
+#pragma unroll
+      for (int e = 0; e < RPL / 2; ++e) p[e] = make_double2(x[2 * e], x[2 * e + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < RPL; ++e)
+      if (r0 + e < TW) m[col * TW + r0 + e] = x[e];
+  }
+}
+
+// pairwise tree over the RPL rows held by one lane (levels 1 .. log2 RPL of
+// the reference tree)
+template <int RPL>
+__device__ __forceinline__ double row_tree(const double (&x)[RPL]) {
+  if constexpr (RPL == 1) {
+    return x[0];
+  } else if constexpr (RPL == 2) {
+    return x[0] + x[1];
+  } else {
+    return (x[0] + x[1]) + (x[2] + x[3]);
+  }
+}
 
 template <int TW, bool CPLX>
 __device__ __forceinline__ void load_col(const double* __restrict__ re, const double* __restrict__ im, int col,
@@ -405,16 +455,15 @@ struct InnerParams {
   int32_t* qr_locks;
 };
 
-template <int TW, bool CPLX, int PPWM>
-__global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(InnerParams P) {
-  using Geo = InnerGeo<TW, CPLX, PPWM>;
+template <int TW, bool CPLX>
+__global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerParams P) {
+  using Geo = InnerGeo<TW, CPLX>;
   constexpr int NPIV = Geo::NPIV;
-  constexpr int NW = Geo::NW;    // warps
-  constexpr int PPW = Geo::PPW;  // pivots per warp and inner step
+  constexpr int NW = Geo::NW;  // warps
   constexpr int EPL = Lanes<TW>::EPL;
   constexpr int NP = CPLX ? 2 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  auto& S = *reinterpret_cast<InnerSmem<TW, CPLX, PPWM>*>(smem_raw);
+  auto& S = *reinterpret_cast<InnerSmem<TW, CPLX>*>(smem_raw);
   const int pair = P.sp.p0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = blockDim.x;
@@ -548,86 +597,85 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(Inn
   if (__syncthreads_or(pbad) && status == ST_OK) status = ST_RANK;
 
   // ---- pointwise sweeps (pointwise.py:222-251) ---------------------------
-  // Per inner step, warp w owns pivots w*PPW .. w*PPW+PPW-1:
-  //   A) forms their six (eight, complex) column dot products with one
-  //      recursive-halving tree and gathers pivot k's sums into lane k;
-  //   B) lane k runs _k_process_pivot's scalar logic for pivot k (gate,
-  //      transform, big / sort decisions) and parks the Z-hat entries in the
-  //      warp's slot of shared memory;
-  //   C) the warp applies the transforms / swaps to its pivots' columns.
-  // Pivots of a step touch disjoint columns, so the only CTA barrier is the
-  // one before the next step reads columns other warps wrote.
+  // Per inner step, lane group g of warp w owns pivot w*PG + g:
+  //   A) its lanes form the six (eight, complex) column dot products over
+  //      their rows and reduce them across the group (pairwise tree);
+  //   B) the group's sub-lane 0 runs _k_process_pivot's scalar logic (gate,
+  //      transform, big / sort decisions) and broadcasts the Z-hat entries;
+  //   C) the group applies the transform / swap to its rows of the columns.
   int total = 0, big = 0, sweeps = 0;
   if (status == ST_OK) {
+    constexpr int RPL = Geo::RPL, LP = Geo::LP, PG = Geo::PG, R = Geo::R;
+    constexpr bool VEC = Geo::VEC;
+    const int grp = lane / LP, sub = lane % LP, base = grp * LP;
+    const int r0 = sub * RPL;
+    const int pv = warp * PG + grp;
+    const bool valid = NPIV % PG == 0 || pv < NPIV;
+    const bool mathlane = sub == 0 && valid;
     const bool prof = P.io.phase != nullptr && blockIdx.x == 0 && tid == 0;
     long long tA = 0, tB = 0, tC = 0, nstep = 0, c0 = 0, c1 = 0;
     for (int sw = 0; sw < kc.max_inner_sweeps; ++sw) {
-      int lane_applied = 0, lane_big = 0;  // lane k: pivot k's counts this sweep
-      // pivot indices of the warp's pivots, fetched one inner step ahead
-      auto fetch = [&](int st, int (&a)[PPW], int (&b)[PPW]) {
-#pragma unroll
-        for (int k = 0; k < PPW; ++k) {
-          const int pv = warp * PPW + k;
-          const bool ok = NPIV % PPW == 0 || pv < NPIV;
-          a[k] = ok ? S.tab[(st * NPIV + pv) * 2] : 0;
-          b[k] = ok ? S.tab[(st * NPIV + pv) * 2 + 1] : 0;
-        }
-      };
-      int nii[PPW], njj[PPW];
-      fetch(0, nii, njj);
+      int lane_applied = 0, lane_big = 0;  // math lanes: the pivot's counts this sweep
+      int ni_ = valid ? S.tab[pv * 2] : 0, nj_ = valid ? S.tab[pv * 2 + 1] : 1;
       for (int st = 0; st < P.isteps; ++st) {
         if (prof) c0 = clock64();
         // ---- phase A
-        int ii[PPW], jj[PPW];
-#pragma unroll
-        for (int k = 0; k < PPW; ++k) {
-          ii[k] = nii[k];
-          jj[k] = njj[k];
+        const int i = ni_, j = nj_;
+        if (st + 1 < P.isteps && valid) {  // next step's pivot, fetched ahead
+          ni_ = S.tab[((st + 1) * NPIV + pv) * 2];
+          nj_ = S.tab[((st + 1) * NPIV + pv) * 2 + 1];
         }
-        fetch(st + 1 < P.isteps ? st + 1 : 0, nii, njj);
-        double fi[PPW][EPL], fii[PPW][EPL], fj[PPW][EPL], fji[PPW][EPL];
-        double gi[PPW][EPL], gii[PPW][EPL], gj[PPW][EPL], gji[PPW][EPL];
-        double v[Geo::QP];
+        double fi[RPL], fj[RPL], gi[RPL], gj[RPL];
+        double fii[RPL], fji[RPL], gii[RPL], gji[RPL];
+        load_rows<TW, VEC, RPL>(Ar, i, r0, fi);
+        load_rows<TW, VEC, RPL>(Ar, j, r0, fj);
+        load_rows<TW, VEC, RPL>(Br, i, r0, gi);
+        load_rows<TW, VEC, RPL>(Br, j, r0, gj);
+        if constexpr (CPLX) {
+          load_rows<TW, VEC, RPL>(Ai, i, r0, fii);
+          load_rows<TW, VEC, RPL>(Ai, j, r0, fji);
+          load_rows<TW, VEC, RPL>(Bi, i, r0, gii);
+          load_rows<TW, VEC, RPL>(Bi, j, r0, gji);
+        } else {
 #pragma unroll
-        for (int q = Geo::Q; q < Geo::QP; ++q) v[q] = 0.0;
+          for (int e = 0; e < RPL; ++e) fii[e] = fji[e] = gii[e] = gji[e] = 0.0;
+        }
+        double v[8];
+        {
+          double p[8][RPL];
 #pragma unroll
-        for (int k = 0; k < PPW; ++k) {
-          load_col<TW, CPLX>(Ar, Ai, ii[k], lane, fi[k], fii[k]);
-          load_col<TW, CPLX>(Ar, Ai, jj[k], lane, fj[k], fji[k]);
-          load_col<TW, CPLX>(Br, Bi, ii[k], lane, gi[k], gii[k]);
-          load_col<TW, CPLX>(Br, Bi, jj[k], lane, gj[k], gji[k]);
-          double p[8][EPL];
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) {
-            p[0][e] = nrm_term<CPLX>(fi[k][e], fii[k][e]);
-            p[1][e] = nrm_term<CPLX>(fj[k][e], fji[k][e]);
-            p[3][e] = nrm_term<CPLX>(gi[k][e], gii[k][e]);
-            p[4][e] = nrm_term<CPLX>(gj[k][e], gji[k][e]);
+          for (int e = 0; e < RPL; ++e) {
+            p[0][e] = nrm_term<CPLX>(fi[e], fii[e]);
+            p[1][e] = nrm_term<CPLX>(fj[e], fji[e]);
+            p[3][e] = nrm_term<CPLX>(gi[e], gii[e]);
+            p[4][e] = nrm_term<CPLX>(gj[e], gji[e]);
             if (CPLX) {
-              p[2][e] = dot_re_term(fi[k][e], fii[k][e], fj[k][e], fji[k][e]);
-              p[6][e] = dot_im_term(fi[k][e], fii[k][e], fj[k][e], fji[k][e]);
-              p[5][e] = dot_re_term(gi[k][e], gii[k][e], gj[k][e], gji[k][e]);
-              p[7][e] = dot_im_term(gi[k][e], gii[k][e], gj[k][e], gji[k][e]);
+              p[2][e] = dot_re_term(fi[e], fii[e], fj[e], fji[e]);
+              p[6][e] = dot_im_term(fi[e], fii[e], fj[e], fji[e]);
+              p[5][e] = dot_re_term(gi[e], gii[e], gj[e], gji[e]);
+              p[7][e] = dot_im_term(gi[e], gii[e], gj[e], gji[e]);
             } else {
-              p[2][e] = fi[k][e] * fj[k][e];
-              p[5][e] = gi[k][e] * gj[k][e];
+              p[2][e] = fi[e] * fj[e];
+              p[5][e] = gi[e] * gj[e];
               p[6][e] = 0.0;
               p[7][e] = 0.0;
             }
           }
 #pragma unroll
-          for (int c = 0; c < 8; ++c) v[k * 8 + c] = EPL == 2 ? p[c][0] + p[c][EPL - 1] : p[c][0];
+          for (int c = 0; c < 8; ++c) v[c] = row_tree<RPL>(p[c]);
         }
-        HalvingTree<Geo::QP, 0>::run(v, lane);
-        // lane k < PPW collects pivot k's eight sums
-        double qv[8];
-        {
-          const int kk = lane < PPW ? lane : 0;
+        HalvingTree<8, 0, Geo::HL>::run(v, lane);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int src = (int)(__brev((unsigned)(kk * 8 + c)) >> (32 - Geo::LQ));
-            qv[c] = __shfl_sync(0xffffffffu, v[0], src);
-          }
+        for (int d = 1 << Geo::HL; d < LP; d <<= 1)
+#pragma unroll
+          for (int s2 = 0; s2 < R; ++s2) v[s2] = v[s2] + __shfl_xor_sync(0xffffffffu, v[s2], d);
+        // the group's sub-lane 0 collects the eight sums
+        double qv[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          int holder = 0;  // sub-lane holding quantity c: rev_HL(c / R)
+          if constexpr (Geo::HL > 0) holder = (int)(__brev((unsigned)(c / R)) >> (32 - Geo::HL));
+          qv[c] = __shfl_sync(0xffffffffu, v[c % R], base + holder);
         }
         if (prof) {
           c1 = clock64();
@@ -635,26 +683,24 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(Inn
           c0 = c1;
         }
         // ---- phase B: _k_process_pivot's scalar part (pointwise.py:165-207)
-        int bad = 0;
-        if (lane < PPW && (NPIV % PPW == 0 || warp * PPW + lane < NPIV)) {
-          double z[6];
+        int flags = 0;
+        double z[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (mathlane) {
           FastMath fm;
-          int flags = pivot_scalar<CPLX>(fm, kc, qv, z);
+          flags = pivot_scalar<CPLX>(fm, kc, qv, z);
           if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
             IeeeMath im;
             flags = pivot_scalar<CPLX>(im, kc, qv, z);
           }
           if (flags & 1) {
-#pragma unroll
-            for (int c = 0; c < 6; ++c) S.wz[warp][lane][c] = z[c];
             lane_applied += 1;
             lane_big += (flags >> 1) & 1;
           }
-          S.wf[warp][lane] = flags;
-          bad = flags & 8;
-        } else if (lane < PPW) {
-          S.wf[warp][lane] = 0;
         }
+        const int bad = flags & 8;
+        flags = __shfl_sync(0xffffffffu, flags, base);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) z[c] = __shfl_sync(0xffffffffu, z[c], base);
         if (st == P.isteps - 1) {
           int sa = lane_applied, sb = lane_big;
 #pragma unroll
@@ -667,34 +713,23 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(Inn
             S.wcnt[warp][1] = sb;
           }
         }
-        __syncwarp();
         if (prof) {
           c1 = clock64();
           tB += c1 - c0;
           c0 = c1;
         }
         // ---- phase C: _k_update_cols / swaps (pointwise.py:178-218)
-        // every shared-memory operand of the warp's pivots is loaded up
-        // front (one latency instead of one per pivot)
-        int fl[PPW];
-        double zz[PPW][6];
-        double zi_[PPW][EPL], zii[PPW][EPL], zj_[PPW][EPL], zji[PPW][EPL];
-#pragma unroll
-        for (int k = 0; k < PPW; ++k) {
-          fl[k] = S.wf[warp][k];
-#pragma unroll
-          for (int c = 0; c < 6; ++c) zz[k][c] = S.wz[warp][k][c];
-          load_col<TW, CPLX>(Zr, Zi, ii[k], lane, zi_[k], zii[k]);
-          load_col<TW, CPLX>(Zr, Zi, jj[k], lane, zj_[k], zji[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < PPW; ++k) {
-          const int i = ii[k], j = jj[k];
-          const int flags = fl[k];
-          bool swap = (flags & 4) != 0;
+        bool swap = (flags & 4) != 0;
+        double zi_[RPL], zj_[RPL], zii[RPL], zji[RPL];
+        if (flags & 5) {
+          load_rows<TW, VEC, RPL>(Zr, i, r0, zi_);
+          load_rows<TW, VEC, RPL>(Zr, j, r0, zj_);
+          if constexpr (CPLX) {
+            load_rows<TW, VEC, RPL>(Zi, i, r0, zii);
+            load_rows<TW, VEC, RPL>(Zi, j, r0, zji);
+          }
           if (flags & 1) {
-            const double z11 = zz[k][0], z12r = zz[k][1], z12i = zz[k][2];
-            const double z21r = zz[k][3], z21i = zz[k][4], z22 = zz[k][5];
+            const double z11 = z[0], z12r = z[1], z12i = z[2], z21r = z[3], z21i = z[4], z22 = z[5];
 #define HZG_UPD(yr, yi, yjr_, yji_)                                                         \
   {                                                                                        \
     double yir = yr[e], yjr = yjr_[e];                                                     \
@@ -712,31 +747,46 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(Inn
     }                                                                                      \
   }
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-              HZG_UPD(fi[k], fii[k], fj[k], fji[k]);
-              HZG_UPD(gi[k], gii[k], gj[k], gji[k]);
-              HZG_UPD(zi_[k], zii[k], zj_[k], zji[k]);
+            for (int e = 0; e < RPL; ++e) {
+              HZG_UPD(fi, fii, fj, fji);
+              HZG_UPD(gi, gii, gj, gji);
+              HZG_UPD(zi_, zii, zj_, zji);
             }
 #undef HZG_UPD
-            if (kc.sorting && CPLX) {
-              double q0[EPL], q1[EPL];
-#pragma unroll
-              for (int e = 0; e < EPL; ++e) {
-                q0[e] = nrm_term<CPLX>(fi[k][e], fii[k][e]);
-                q1[e] = nrm_term<CPLX>(fj[k][e], fji[k][e]);
-              }
-              double ni = lane_tree<EPL>(q0), nj = lane_tree<EPL>(q1);
-              swap = ni < nj;
-            }
           }
-          if (flags & 1 || swap) {
-            const int di = swap ? j : i, dj = swap ? i : j;
-            store_col<TW, CPLX>(Ar, Ai, di, lane, fi[k], fii[k]);
-            store_col<TW, CPLX>(Ar, Ai, dj, lane, fj[k], fji[k]);
-            store_col<TW, CPLX>(Br, Bi, di, lane, gi[k], gii[k]);
-            store_col<TW, CPLX>(Br, Bi, dj, lane, gj[k], gji[k]);
-            store_col<TW, CPLX>(Zr, Zi, di, lane, zi_[k], zii[k]);
-            store_col<TW, CPLX>(Zr, Zi, dj, lane, zj_[k], zji[k]);
+        }
+        if (CPLX && kc.sorting) {
+          // complex sort: recompute the squared norms after the update
+          // (pointwise.py:211-214); every lane takes part in the shuffles
+          double q0[RPL], q1[RPL];
+#pragma unroll
+          for (int e = 0; e < RPL; ++e) {
+            q0[e] = nrm_term<CPLX>(fi[e], fii[e]);
+            q1[e] = nrm_term<CPLX>(fj[e], fji[e]);
+          }
+          double ni = row_tree<RPL>(q0), nj = row_tree<RPL>(q1);
+#pragma unroll
+          for (int d = 1; d < LP; d <<= 1) {
+            ni = ni + __shfl_xor_sync(0xffffffffu, ni, d);
+            nj = nj + __shfl_xor_sync(0xffffffffu, nj, d);
+          }
+          if (flags & 1) swap = ni < nj;
+        }
+        if (flags & 5) {
+          const int di = swap ? j : i, dj = swap ? i : j;
+          store_rows<TW, VEC, RPL>(Ar, di, r0, fi);
+          store_rows<TW, VEC, RPL>(Ar, dj, r0, fj);
+          store_rows<TW, VEC, RPL>(Br, di, r0, gi);
+          store_rows<TW, VEC, RPL>(Br, dj, r0, gj);
+          store_rows<TW, VEC, RPL>(Zr, di, r0, zi_);
+          store_rows<TW, VEC, RPL>(Zr, dj, r0, zj_);
+          if constexpr (CPLX) {
+            store_rows<TW, VEC, RPL>(Ai, di, r0, fii);
+            store_rows<TW, VEC, RPL>(Ai, dj, r0, fji);
+            store_rows<TW, VEC, RPL>(Bi, di, r0, gii);
+            store_rows<TW, VEC, RPL>(Bi, dj, r0, gji);
+            store_rows<TW, VEC, RPL>(Zi, di, r0, zii);
+            store_rows<TW, VEC, RPL>(Zi, dj, r0, zji);
           }
         }
         // a rank-deficient pivot anywhere ends the solve (RankError upstream)
@@ -822,30 +872,16 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX, PPWM>::NW * 32) k_inner(Inn
   }
 }
 
-template <int TW, bool CPLX, int PPWM>
-int launch_inner_g(const InnerParams& p, cudaStream_t s) {
-  const size_t smem = sizeof(InnerSmem<TW, CPLX, PPWM>);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_inner<TW, CPLX, PPWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_done = true;
-  }
-  k_inner<TW, CPLX, PPWM><<<p.sp.pn, InnerGeo<TW, CPLX, PPWM>::NW * 32, smem, s>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
-}
-
 template <int TW, bool CPLX>
 int launch_inner_t(const InnerParams& p, cudaStream_t s) {
-  if constexpr (TW == 32 && !CPLX) {
-    // pivots per warp (HZG_PPW=2 selects 8 warps x 2 pivots; for tuning)
-    static int ppw = -1;
-    if (ppw < 0) {
-      const char* e = std::getenv("HZG_PPW");
-      ppw = e ? std::atoi(e) : 4;
-    }
-    if (ppw == 2) return launch_inner_g<TW, CPLX, 2>(p, s);
+  const size_t smem = sizeof(InnerSmem<TW, CPLX>);
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(k_inner<TW, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_done = true;
   }
-  return launch_inner_g<TW, CPLX, 0>(p, s);
+  k_inner<TW, CPLX><<<p.sp.pn, InnerGeo<TW, CPLX>::NW * 32, smem, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 }  // namespace
