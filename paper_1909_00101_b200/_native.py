@@ -11,7 +11,7 @@ import threading
 from .errors import DeviceError, NotPositiveDefiniteError, RankError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libhzg.so")
+LIB_PATH = os.environ.get("HZG_LIB") or os.path.join(HERE, "_lib", "libhzg.so")
 
 HZG_OK, HZG_RANK, HZG_NOT_PD, HZG_CUDA, HZG_INVALID = 0, 1, 2, 3, 4
 

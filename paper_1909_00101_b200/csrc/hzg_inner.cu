@@ -685,7 +685,17 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
         // ---- phase B: _k_process_pivot's scalar part (pointwise.py:165-207)
         int flags = 0;
         double z[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#ifdef HZG_EXP_NOMATH
+        if (mathlane) {  // experiment: every pivot applies the identity (no 2x2 math)
+          flags = 1;
+          z[0] = 1.0;
+          z[5] = 1.0;
+          lane_applied += 1;
+        }
+        if (false) {
+#else
         if (mathlane) {
+#endif
           FastMath fm;
           flags = pivot_scalar<CPLX>(fm, kc, qv, z);
           if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
