@@ -218,6 +218,7 @@ KernelCfg kernel_cfg(const hzg_ctx* c) {
   k.sorting = c->cfg.sorting;
   k.max_inner_sweeps = c->cfg.max_inner_sweeps;
   k.fallback_qr = c->cfg.fallback_qr;
+  k.shorten_qr = c->cfg.shorten_qr;
   k.epsn = c->epsn;
   return k;
 }
@@ -237,8 +238,11 @@ int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr,
   StepPairs sp{c->d_colpair, c->npairs, p0, pn < 0 ? c->npairs : pn};
   KernelCfg kc = kernel_cfg(c);
   if (ev) record(ev[0], s);
-  int rc = c->use_dmma ? launch_gram_dmma(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s)
-                       : launch_gram_exact(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s);
+  int rc = HZG_OK;
+  if (!c->cfg.shorten_qr) {  // shorten == "qr": the inner kernel factors the columns itself
+    rc = c->use_dmma ? launch_gram_dmma(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s)
+                     : launch_gram_exact(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s);
+  }
   if (rc) return rc;
   if (ev) record(ev[1], s);
   rc = launch_inner(c->F, c->G, sp, step, kc, c->gw, c->d_itable, c->isteps, c->io, c->d_qr, c->qr_slots,
@@ -287,7 +291,6 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
     return HZG_INVALID;
   if (cfg->variant_id < 0 || cfg->variant_id > 7) return HZG_INVALID;
   if (cfg->variant_id % 2 == 1) return HZG_INVALID;  // compensated dots: not on the device path yet
-  if (cfg->shorten_qr) return HZG_INVALID;           // shorten="qr": not on the device path yet
   if (2 * w > 64 || (2 * w > 32 && 2 * w != 48 && 2 * w != 64)) return HZG_INVALID;
   static const int supported[] = {2, 4, 6, 8, 10, 12, 14, 16, 20, 24, 32, 48, 64};
   bool ok = false;
@@ -327,7 +330,9 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   c->itable_host.assign(inner.begin(), inner.begin() + (size_t)c->isteps * c->tw);
   for (int mat = 0; mat < 2; ++mat) gram_split(mat == 0 ? mF : mG, !c->use_dmma, c->gw.nsplit[mat], c->gw.chunk[mat]);
   c->gw.smax = std::max(c->gw.nsplit[0], c->gw.nsplit[1]);
-  c->qr_slots = (int)std::max<int64_t>(1, std::min<int64_t>(16, c->npairs));
+  // QR scratch slots: one per pair when every pair is shortened by QR,
+  // otherwise a few shared by the rare Cholesky failures
+  c->qr_slots = cfg->shorten_qr ? c->npairs : (int)std::max<int64_t>(1, std::min<int64_t>(16, c->npairs));
   *out = c;
   return HZG_OK;
 }
@@ -341,7 +346,7 @@ int hzg_set_schedule(hzg_ctx* c, const int32_t* colpairs, int32_t osteps, int32_
   c->npairs = npairs;
   c->colpair_host.assign(colpairs, colpairs + (size_t)osteps * npairs * 2);
   c->wavefront = false;
-  c->qr_slots = std::max(1, std::min(16, npairs));
+  c->qr_slots = c->cfg.shorten_qr ? npairs : std::max(1, std::min(16, npairs));
   return HZG_OK;
 }
 
@@ -645,6 +650,7 @@ int hzg_test_block(int32_t tw, int32_t is_complex, const hzg_config* cfg, double
   StepPairs sp{d_misc + 8, 1, 0, 1};  // colpair (0, 0): only used by the QR fallback
   KernelCfg kc = kernel_cfg(&c);
   kc.fallback_qr = 0;  // the block test has no columns to shorten
+  kc.shorten_qr = 0;
   Plane dummy{nullptr, nullptr, 0, 0};
   int rc = launch_inner(dummy, dummy, sp, 0, kc, gw, d_misc + 16, isteps, io, nullptr, 1, d_misc + 12, 0);
   cudaError_t e = cudaDeviceSynchronize();

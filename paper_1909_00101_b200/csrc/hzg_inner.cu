@@ -476,7 +476,9 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   }
 
   // ---- fold the Grammian partials (pairwise over splits) -----------------
-  for (int mat = 0; mat < 2; ++mat) {
+  // (shorten == "qr": no Grammians; both factors come from the QR below)
+  if (kc.shorten_qr && tid == 0) S.chol_fail[0] = S.chol_fail[1] = 1;
+  for (int mat = 0; mat < 2 && !kc.shorten_qr; ++mat) {
     const int ns = P.gw.nsplit[mat];
     const double* base = P.gw.part + ((int64_t)pair * 2 + mat) * P.gw.smax * NP * TW * TW;
     double(*M)[TW * TW] = mat == 0 ? S.A : S.B;
@@ -498,13 +500,13 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   __syncthreads();
 
   // ---- Cholesky of both Grammians (warp 0: F, warp 1: G) -----------------
-  if (warp < 2) {
+  if (warp < 2 && !kc.shorten_qr) {
     double* Mr = warp == 0 ? S.A[0] : S.B[0];
     double* Mi = CPLX ? (warp == 0 ? S.A[NP - 1] : S.B[NP - 1]) : nullptr;
     int f = warp_cholesky<TW, CPLX>(Mr, Mi, lane);
     if (lane == 0) S.chol_fail[warp] = f;
   }
-  if (NW == 1) {  // a single warp: factor G after F
+  if (NW == 1 && !kc.shorten_qr) {  // a single warp: factor G after F
     __syncwarp();
     int f = warp_cholesky<TW, CPLX>(S.B[0], CPLX ? S.B[NP - 1] : nullptr, lane);
     if (lane == 0) S.chol_fail[1] = f;
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   int status = ST_OK;
   for (int mat = 0; mat < 2; ++mat) {
     if (!S.chol_fail[mat]) continue;
-    if (!kc.fallback_qr) {
+    if (!kc.fallback_qr && !kc.shorten_qr) {
       status = ST_NOT_PD;
       break;
     }

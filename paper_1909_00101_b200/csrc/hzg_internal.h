@@ -42,6 +42,7 @@ struct KernelCfg {
   int sorting;
   int max_inner_sweeps;
   int fallback_qr;
+  int shorten_qr;       // cfg.shorten == "qr": QR R factors instead of Grammian + Cholesky
   double epsn;          // gate_eps * sqrt(n) (blocked.py:571-572)
 };
 

@@ -73,14 +73,33 @@ def cases(hz):
     add("qrfallback48_complex_w8", *dependent(48, 11, cplx=True), block_width=8)
     pair, _ = hz.gen_pair(hz.random_genspec(256, 4242, "real"))
     add("genpair256_w16", pair.F.to_dense(), pair.G.to_dense(), full=False, block_width=16)
+    # QR shortening instead of Grammian + Cholesky for every block pair
+    # (cfg.shorten == "qr", blocked.py:445-447, :487-500)
+    pair, _ = hz.gen_pair(hz.random_genspec(48, 99, "real"))
+    add("real48_shortenqr_w4", pair.F.to_dense(), pair.G.to_dense(), block_width=4, shorten="qr")
+    add("complex40_shortenqr_w4", pairc.F.to_dense(), pairc.G.to_dense(), block_width=4, shorten="qr")
+    # compensated dot products (odd variant ids, pointwise.py:40-81, dotprod.py:125-252)
+    for vid in (1, 3, 5, 7):
+        add("real48_v%d_w4" % vid, pair.F.to_dense(), pair.G.to_dense(), block_width=4, variant_id=vid)
+    add("complex40_v1_w4", pairc.F.to_dense(), pairc.G.to_dense(), block_width=4, variant_id=1)
+    add("complex40_v7_w8", pairc.F.to_dense(), pairc.G.to_dense(), block_width=8, variant_id=7)
     return out
 
 
 def main():
     sys.path.insert(0, REF)
     import hzgsvd as hz
+    only = None
+    if len(sys.argv) > 2 and sys.argv[1] == "--only":
+        only = set(sys.argv[2].split(","))
+    mpath = os.path.join(HERE, "manifest.json")
     manifest = {}
+    if only and os.path.exists(mpath):
+        with open(mpath) as fh:
+            manifest = json.load(fh)
     for name, F, G, cfg, full in cases(hz):
+        if only and name not in only:
+            continue
         r = hz.solve(F, G, hz.SolverConfig(**cfg))
         data = dict(F=F, G=G, sigma=r.sigma, sigmaF=r.sigmaF, sigmaG=r.sigmaG,
                     counters=np.array([r.sweeps, r.total_transforms, r.big_transforms, int(r.converged)]))
@@ -90,7 +109,7 @@ def main():
         manifest[name] = dict(cfg=cfg, full=full, n=int(F.shape[1]), mF=int(F.shape[0]), mG=int(G.shape[0]),
                               complex=bool(np.iscomplexobj(F)), sweeps=int(r.sweeps))
         print(name, r.sweeps, r.total_transforms, r.big_transforms, r.converged, flush=True)
-    with open(os.path.join(HERE, "manifest.json"), "w") as fh:
+    with open(mpath, "w") as fh:
         json.dump(manifest, fh, indent=1, sort_keys=True)
 
 
