@@ -28,6 +28,8 @@ struct hzg_ctx {
   int w = 0, tw = 0, nblk = 0;
   int osteps = 0, npairs = 0, isteps = 0;
   bool use_dmma = false;
+  bool comp = false;        // compensated dot products (odd variant ids)
+  int64_t cstride = 0;      // doubles of compensated scratch per column / per thread (pow2 of the height)
   bool wavefront = false;   // schedule in circle-position order (ME)
   int groups = 1;           // position groups of the wavefront sweep graph
   std::vector<cudaStream_t> gstreams;
@@ -52,6 +54,7 @@ struct hzg_ctx {
   int qr_slots = 0;
   int32_t* d_fin = nullptr;    // 2n int32
   double* d_sig = nullptr;     // 3n
+  double* d_comp = nullptr;    // compensated-variant scratch
   int64_t* h_ctr = nullptr;    // pinned
   long long* d_phase = nullptr;
   std::string err;
@@ -176,7 +179,7 @@ void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
 }
 
 struct Layout {
-  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, phase, total;
+  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, phase, comp, total;
 };
 
 Layout layout(const hzg_ctx* c) {
@@ -202,6 +205,12 @@ Layout layout(const hzg_ctx* c) {
   L.fin = take((size_t)2 * c->n * 4);
   L.sig = take((size_t)3 * c->n * 8);
   L.phase = take(4 * 8);
+  // compensated variants: per-column scratch for the full-height norms and
+  // per-thread scratch for the Grammian entries (32 threads per pair, matrix)
+  size_t cs = 0;
+  if (c->comp)
+    cs = (size_t)c->cstride * 8 * std::max<size_t>((size_t)c->n, (size_t)c->npairs * 2 * 32);
+  L.comp = take(cs);
   L.total = off;
   return L;
 }
@@ -239,7 +248,11 @@ int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr,
   KernelCfg kc = kernel_cfg(c);
   if (ev) record(ev[0], s);
   int rc = HZG_OK;
-  if (!c->cfg.shorten_qr) {  // shorten == "qr": the inner kernel factors the columns itself
+  if (c->cfg.shorten_qr) {
+    // shorten == "qr": the inner kernel factors the columns itself
+  } else if (c->comp) {
+    rc = launch_gram_comp(c->F, c->G, sp, step, c->w, c->cplx, c->gw, c->d_comp, c->cstride, s);
+  } else {
     rc = c->use_dmma ? launch_gram_dmma(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s)
                      : launch_gram_exact(c->F, c->G, sp, step, c->w, c->cplx, c->gw, s);
   }
@@ -290,7 +303,6 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   if (w < 1 || n < 2 * w || n % (2 * w) != 0 || mF % (2 * w) != 0 || mG % (2 * w) != 0 || mF < 1 || mG < 1)
     return HZG_INVALID;
   if (cfg->variant_id < 0 || cfg->variant_id > 7) return HZG_INVALID;
-  if (cfg->variant_id % 2 == 1) return HZG_INVALID;  // compensated dots: not on the device path yet
   if (2 * w > 64 || (2 * w > 32 && 2 * w != 48 && 2 * w != 64)) return HZG_INVALID;
   static const int supported[] = {2, 4, 6, 8, 10, 12, 14, 16, 20, 24, 32, 48, 64};
   bool ok = false;
@@ -311,6 +323,8 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   c->nblk = (int)(n / w);
   c->npairs = c->nblk / 2;
   c->use_dmma = !cfg->exact && dmma_supported(w);
+  c->comp = cfg->variant_id % 2 == 1;
+  c->cstride = pow2c(std::max(std::max(mF, mG), n));
   std::vector<int32_t> outer;
   if (cfg->outer_mm) {
     c->osteps = gen_table(true, c->nblk, outer);
@@ -329,7 +343,13 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   c->isteps = gen_table(cfg->inner_mm != 0, c->tw, inner);
   c->itable_host.assign(inner.begin(), inner.begin() + (size_t)c->isteps * c->tw);
   for (int mat = 0; mat < 2; ++mat) gram_split(mat == 0 ? mF : mG, !c->use_dmma, c->gw.nsplit[mat], c->gw.chunk[mat]);
+  if (c->comp) {  // the compensated Grammian is one sequential form over the full height
+    c->gw.nsplit[0] = c->gw.nsplit[1] = 1;
+    c->gw.chunk[0] = mF;
+    c->gw.chunk[1] = mG;
+  }
   c->gw.smax = std::max(c->gw.nsplit[0], c->gw.nsplit[1]);
+
   // QR scratch slots: one per pair when every pair is shortened by QR,
   // otherwise a few shared by the rare Cholesky failures
   c->qr_slots = cfg->shorten_qr ? c->npairs : (int)std::max<int64_t>(1, std::min<int64_t>(16, c->npairs));
@@ -375,6 +395,7 @@ int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double*
   c->d_fin = (int32_t*)(c->ws + L.fin);
   c->d_sig = (double*)(c->ws + L.sig);
   c->d_phase = (long long*)(c->ws + L.phase);
+  c->d_comp = c->comp ? (double*)(c->ws + L.comp) : nullptr;
   c->io.phase = nullptr;
   if ((e = cudaMemcpyAsync(c->d_colpair, c->colpair_host.data(), c->colpair_host.size() * 4,
                            cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
@@ -412,7 +433,8 @@ int hzg_init_fgz(hzg_ctx* c) {
   if (c->Z.im) cudaMemsetAsync(c->Z.im, 0, zb, c->stream);
   cudaMemsetAsync(c->d_status, 0, 16, c->stream);
   KernelCfg kc = kernel_cfg(c);
-  int rc = launch_prescale(c->F, c->G, c->Z, c->n, c->cplx, kc.prescale, c->d_status, c->stream);
+  int rc = launch_prescale(c->F, c->G, c->Z, c->n, c->cplx, kc.prescale, c->d_status, c->comp ? c->d_comp : nullptr,
+                           c->cstride, c->stream);
   if (rc) return fail(c, rc, "prescale launch");
   int32_t st = 0;
   if ((e = cudaMemcpyAsync(c->h_ctr, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
@@ -484,7 +506,7 @@ static int build_graph(hzg_ctx* c) {
   if (rc == HZG_OK) rc = launch_counters(c->io.counts, (int64_t)c->osteps * c->npairs, c->d_ctr, c->cap);
   if (rc == HZG_OK)
     rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 0, nullptr, nullptr, nullptr, c->d_ctr, c->d_status,
-                        c->cap);
+                        c->comp ? c->d_comp : nullptr, c->cstride, c->cap);
   cudaGraph_t g = nullptr;
   e = cudaStreamEndCapture(c->cap, &g);
   if (rc != HZG_OK) {
@@ -578,7 +600,7 @@ int hzg_collect(hzg_ctx* c, int64_t* total, int64_t* big) {
 int hzg_rescale_z(hzg_ctx* c) {
   if (!c || !c->bound) return HZG_INVALID;
   int rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 0, nullptr, nullptr, nullptr, nullptr, c->d_status,
-                          c->stream);
+                          c->comp ? c->d_comp : nullptr, c->cstride, c->stream);
   return rc ? fail(c, rc, "rescale launch") : HZG_OK;
 }
 
@@ -590,7 +612,8 @@ int hzg_finalize(hzg_ctx* c, int64_t n0, int64_t mF0, int64_t mG0, int32_t sort,
   double* sG = sF + c->n;
   double* s = sG + c->n;
   cudaMemsetAsync(c->d_status, 0, 16, c->stream);
-  int rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 1, sF, sG, s, nullptr, c->d_status, c->stream);
+  int rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 1, sF, sG, s, nullptr, c->d_status,
+                          c->comp ? c->d_comp : nullptr, c->cstride, c->stream);
   if (rc) return fail(c, rc, "final rescale launch");
   if ((e = cudaMemcpyAsync(c->h_ctr, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
     return cuda_fail(c, e, "status copy");

@@ -43,6 +43,7 @@ struct InnerGeo {
   static constexpr int HL = LV < 3 ? LV : 3;    // halving levels over the 8 quantities
   static constexpr int R = 8 >> HL;             // quantities per lane after halving
   static constexpr bool VEC = TW % 4 == 0 && RPL == 4;  // 16-byte shared loads / stores
+  static constexpr int NCB = NPIV > NW ? NPIV : NW;     // compensated-variant scratch slots
 };
 
 template <int TW, bool CPLX>
@@ -55,6 +56,7 @@ struct InnerSmem {
   uint8_t tab[TW * TW];               // inner table, (steps, TW/2, 2)
   int wcnt[Geo::NW][2];               // per-warp sweep counters (applied, big)
   int chol_fail[2];
+  double cbuf[Geo::NCB][Geo::LT];     // compensated variants: sequential tree scratch per pivot / warp
 };
 
 // Pairwise tree over NS (a power of two) strided values: the split
@@ -571,9 +573,16 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
       if (kc.prescale) {
         double br[EPL], bi[EPL], p[EPL];
         load_col<TW, CPLX>(Br, Bi, c, lane, br, bi);
+        double ng2;
+        if (kc.compensated) {  // _k_col_norm with comp (pointwise.py:260)
+          double v = 0.0;
+          if (lane == 0) v = ccol_norm(Br + c * TW, CPLX ? Bi + c * TW : nullptr, TW, S.cbuf[warp]);
+          ng2 = __shfl_sync(0xffffffffu, v, 0);
+        } else {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) p[e] = nrm_term<CPLX>(br[e], bi[e]);
-        double ng2 = lane_tree<EPL>(p);
+          for (int e = 0; e < EPL; ++e) p[e] = nrm_term<CPLX>(br[e], bi[e]);
+          ng2 = lane_tree<EPL>(p);
+        }
         if (!(ng2 > 0.0)) {
           pbad = 1;
         } else {
@@ -642,6 +651,22 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
 #pragma unroll
           for (int e = 0; e < RPL; ++e) fii[e] = fji[e] = gii[e] = gji[e] = 0.0;
         }
+        double qv[8];  // sub-lane 0 of the group: the pivot's eight sums
+        if (kc.compensated) {
+          // compensated variants: the math lane forms the six (eight) sums
+          // with the reference's sequential compensated trees (pointwise.py:165-170)
+          if (mathlane) {
+            double* cb = S.cbuf[pv];
+            qv[0] = ccol_norm(Ar + i * TW, CPLX ? Ai + i * TW : nullptr, TW, cb);
+            qv[1] = ccol_norm(Ar + j * TW, CPLX ? Ai + j * TW : nullptr, TW, cb);
+            ccol_dot(Ar + i * TW, CPLX ? Ai + i * TW : nullptr, Ar + j * TW, CPLX ? Ai + j * TW : nullptr, TW, cb,
+                     qv[2], qv[6]);
+            qv[3] = ccol_norm(Br + i * TW, CPLX ? Bi + i * TW : nullptr, TW, cb);
+            qv[4] = ccol_norm(Br + j * TW, CPLX ? Bi + j * TW : nullptr, TW, cb);
+            ccol_dot(Br + i * TW, CPLX ? Bi + i * TW : nullptr, Br + j * TW, CPLX ? Bi + j * TW : nullptr, TW, cb,
+                     qv[5], qv[7]);
+          }
+        } else {
         double v[8];
         {
           double p[8][RPL];
@@ -672,12 +697,12 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
 #pragma unroll
           for (int s2 = 0; s2 < R; ++s2) v[s2] = v[s2] + __shfl_xor_sync(0xffffffffu, v[s2], d);
         // the group's sub-lane 0 collects the eight sums
-        double qv[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           int holder = 0;  // sub-lane holding quantity c: rev_HL(c / R)
           if constexpr (Geo::HL > 0) holder = (int)(__brev((unsigned)(c / R)) >> (32 - Geo::HL));
           qv[c] = __shfl_sync(0xffffffffu, v[c % R], base + holder);
+        }
         }
         if (prof) {
           c1 = clock64();
@@ -767,7 +792,27 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
 #undef HZG_UPD
           }
         }
-        if (CPLX && kc.sorting) {
+        if (CPLX && kc.sorting && kc.compensated) {
+          // complex sort, compensated norms of the updated columns
+          // (pointwise.py:211-214): park the updated F columns, let the
+          // math lane read them whole
+          if (flags & 1) {
+            store_rows<TW, VEC, RPL>(Ar, i, r0, fi);
+            store_rows<TW, VEC, RPL>(Ar, j, r0, fj);
+            store_rows<TW, VEC, RPL>(Ai, i, r0, fii);
+            store_rows<TW, VEC, RPL>(Ai, j, r0, fji);
+          }
+          __syncwarp();
+          int sw_ = 0;
+          if (mathlane && (flags & 1)) {
+            const double ni = ccol_norm(Ar + i * TW, Ai + i * TW, TW, S.cbuf[pv]);
+            const double nj = ccol_norm(Ar + j * TW, Ai + j * TW, TW, S.cbuf[pv]);
+            sw_ = ni < nj;
+          }
+          sw_ = __shfl_sync(0xffffffffu, sw_, base);
+          if (flags & 1) swap = sw_ != 0;
+          __syncwarp();
+        } else if (CPLX && kc.sorting) {
           // complex sort: recompute the squared norms after the update
           // (pointwise.py:211-214); every lane takes part in the shuffles
           double q0[RPL], q1[RPL];
@@ -845,6 +890,13 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
         q[e] = nrm_term<CPLX>(br[e], bi[e]);
       }
       double s = lane_tree<EPL>(p) + lane_tree<EPL>(q);
+      if (kc.compensated) {  // pointwise.py:283-284 with comp
+        double v = 0.0;
+        if (lane == 0)
+          v = ccol_norm(Ar + c * TW, CPLX ? Ai + c * TW : nullptr, TW, S.cbuf[warp]) +
+              ccol_norm(Br + c * TW, CPLX ? Bi + c * TW : nullptr, TW, S.cbuf[warp]);
+        s = __shfl_sync(0xffffffffu, v, 0);
+      }
       if (!(s > 0.0)) {
         tbad = 1;
       } else {

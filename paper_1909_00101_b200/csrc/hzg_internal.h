@@ -63,10 +63,14 @@ struct InnerOut {
 };
 
 // kernel launchers (hzg_kernels.cu / hzg_dmma.cu)
+// cscr (compensated variants): per-column scratch of cstride doubles, or nullptr
 int launch_prescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, int cplx, int do_prescale,
-                    int32_t* status, cudaStream_t s);
+                    int32_t* status, double* cscr, int64_t cstride, cudaStream_t s);
 int launch_rescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, int cplx, int final, double* sigF,
-                   double* sigG, double* sig, const int64_t* gate_counters, int32_t* status, cudaStream_t s);
+                   double* sigG, double* sig, const int64_t* gate_counters, int32_t* status, double* cscr,
+                   int64_t cstride, cudaStream_t s);
+int launch_gram_comp(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
+                     const GramWS& gw, double* scratch, int64_t pstride, cudaStream_t s);
 int launch_gram_exact(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
                       const GramWS& gw, cudaStream_t s);
 int launch_gram_dmma(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,

@@ -67,14 +67,28 @@ __device__ __forceinline__ void scale_col(double* re, double* im, int64_t rows, 
 
 // pointwise.py:254-274 over the full pair (blocked.py:564-570); Z is zero
 // on entry and receives diag(z0).
-__global__ void __launch_bounds__(kNT) k_prescale(Plane F, Plane G, Plane Z, int do_prescale, int32_t* status) {
+// Squared column norm over the full height: the reference tree by the whole
+// block, or (cscr != nullptr: compensated variants) the reference's
+// sequential compensated form by thread 0 on the column's scratch.
+__device__ double col_norm_full(const double* re, const double* im, int64_t rows, double* red, double* cscr) {
+  if (!cscr) return block_tree(NormTerm{re, im}, rows, red);
+  __syncthreads();
+  if (threadIdx.x == 0) red[0] = ccol_norm(re, im, rows, cscr);
+  __syncthreads();
+  const double v = red[0];
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(kNT) k_prescale(Plane F, Plane G, Plane Z, int do_prescale, int32_t* status,
+                                                  double* cscr, int64_t cstride) {
   __shared__ double red[kNT / 32];
   const int64_t j = blockIdx.x;
   double z = 1.0;
   if (do_prescale) {
     double* gr = G.re + j * G.ld;
     double* gi = G.im ? G.im + j * G.ld : nullptr;
-    double ng2 = block_tree(NormTerm{gr, gi}, G.rows, red);
+    double ng2 = col_norm_full(gr, gi, G.rows, red, cscr ? cscr + j * cstride : nullptr);
     if (!(ng2 > 0.0)) {
       if (threadIdx.x == 0) atomicOr(status, ST_RANK);
       return;
@@ -92,7 +106,8 @@ __global__ void __launch_bounds__(kNT) k_prescale(Plane F, Plane G, Plane Z, int
 // rescale only runs when the sweep applied big transforms and saw no error
 // (the reference breaks before rescaling on convergence, blocked.py:537-542).
 __global__ void __launch_bounds__(kNT) k_rescale(Plane F, Plane G, Plane Z, int final, double* sigF, double* sigG,
-                                                 double* sig, const int64_t* gate, int32_t* status) {
+                                                 double* sig, const int64_t* gate, int32_t* status, double* cscr,
+                                                 int64_t cstride) {
   __shared__ double red[kNT / 32];
   if (gate && (gate[1] == 0 || gate[2] != 0)) return;
   const int64_t j = blockIdx.x;
@@ -100,8 +115,9 @@ __global__ void __launch_bounds__(kNT) k_rescale(Plane F, Plane G, Plane Z, int 
   double* fi = F.im ? F.im + j * F.ld : nullptr;
   double* gr = G.re + j * G.ld;
   double* gi = G.im ? G.im + j * G.ld : nullptr;
-  double nf2 = block_tree(NormTerm{fr, fi}, F.rows, red);
-  double ng2 = block_tree(NormTerm{gr, gi}, G.rows, red);
+  double* cs = cscr ? cscr + j * cstride : nullptr;
+  double nf2 = col_norm_full(fr, fi, F.rows, red, cs);
+  double ng2 = col_norm_full(gr, gi, G.rows, red, cs);
   double sf = 0.0, sg = 0.0;
   if (final) {
     if (!(nf2 > 0.0 && ng2 > 0.0)) {
@@ -183,6 +199,49 @@ __global__ void __launch_bounds__(256) k_gram_exact(GramExactParams P) {
       out[e] = vr;
       if (P.cplx) out[ne + e] = vi;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// compensated Grammian (odd variant ids; blocked.py:40-56 with comp): one
+// thread per upper entry, the reference's sequential compensated forms over
+// the full height on a per-thread scratch of pow2(m) doubles.  Written as
+// the single split of the partials.
+// ---------------------------------------------------------------------------
+constexpr int kGramCompNT = 32;
+
+struct GramCompParams {
+  Plane Y[2];
+  StepPairs sp;
+  int step, w, cplx;
+  GramWS gw;
+  double* scratch;
+  int64_t pstride;
+};
+
+__global__ void __launch_bounds__(kGramCompNT) k_gram_comp(GramCompParams P) {
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y;
+  const Plane& Y = P.Y[mat];
+  const int w = P.w, tw = 2 * w, NP = P.cplx ? 2 : 1;
+  const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
+  double* out = P.gw.part + ((int64_t)pair * 2 + mat) * P.gw.smax * NP * tw * tw;
+  double* buf = P.scratch + (((int64_t)pair * 2 + mat) * kGramCompNT + threadIdx.x) * P.pstride;
+  const int ne = tw * tw;
+  for (int e = threadIdx.x; e < ne; e += kGramCompNT) {
+    const int r = e % tw, s = e / tw;
+    if (r > s) continue;
+    const int64_t cr = r < w ? cp[0] + r : cp[1] + (r - w);
+    const int64_t cs = s < w ? cp[0] + s : cp[1] + (s - w);
+    const double* ar = Y.re + cr * Y.ld;
+    const double* ai = Y.im ? Y.im + cr * Y.ld : nullptr;
+    double vr, vi = 0.0;
+    if (r == s) {
+      vr = ccol_norm(ar, ai, Y.rows, buf);
+    } else {
+      ccol_dot(ar, ai, Y.re + cs * Y.ld, Y.im ? Y.im + cs * Y.ld : nullptr, Y.rows, buf, vr, vi);
+    }
+    out[e] = vr;
+    if (P.cplx) out[ne + e] = vi;
   }
 }
 
@@ -425,16 +484,17 @@ int fastmath_check(int64_t n, uint64_t seed, int64_t* out4) {
 }
 
 int launch_prescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, int cplx, int do_prescale,
-                    int32_t* status, cudaStream_t s) {
+                    int32_t* status, double* cscr, int64_t cstride, cudaStream_t s) {
   (void)cplx;
-  k_prescale<<<(unsigned)n, kNT, 0, s>>>(F, G, Z, do_prescale, status);
+  k_prescale<<<(unsigned)n, kNT, 0, s>>>(F, G, Z, do_prescale, status, cscr, cstride);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 int launch_rescale(const Plane& F, const Plane& G, const Plane& Z, int64_t n, int cplx, int final, double* sigF,
-                   double* sigG, double* sig, const int64_t* gate, int32_t* status, cudaStream_t s) {
+                   double* sigG, double* sig, const int64_t* gate, int32_t* status, double* cscr, int64_t cstride,
+                   cudaStream_t s) {
   (void)cplx;
-  k_rescale<<<(unsigned)n, kNT, 0, s>>>(F, G, Z, final, sigF, sigG, sig, gate, status);
+  k_rescale<<<(unsigned)n, kNT, 0, s>>>(F, G, Z, final, sigF, sigG, sig, gate, status, cscr, cstride);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -472,6 +532,14 @@ int launch_postmult_exact(const Plane& F, const Plane& G, const Plane& Z, const 
       return 4;
   }
 #undef HZG_CASE
+}
+
+int launch_gram_comp(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
+                     const GramWS& gw, double* scratch, int64_t pstride, cudaStream_t s) {
+  GramCompParams p{{F, G}, sp, step, w, cplx, gw, scratch, pstride};
+  dim3 grid(sp.pn, 2, 1);
+  k_gram_comp<<<grid, kGramCompNT, 0, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 int launch_counters(const int32_t* counts, int64_t nentries, int64_t* out, cudaStream_t s) {

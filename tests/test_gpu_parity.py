@@ -34,15 +34,9 @@ def _cfg(c, **kw):
 # exact mode: bitwise against the reference's own outputs
 # ---------------------------------------------------------------------------
 
-def _skip_unsupported(c):
-    if c["cfg"].get("variant_id", 0) % 2 == 1:
-        pytest.skip("compensated dot products (odd variant ids) are not on the device path yet")
-
-
 @pytest.mark.parametrize("name", CASES)
 def test_exact_mode_bitwise_vs_reference(name):
     c = load_case(name)
-    _skip_unsupported(c)
     r = hz.solve(c["F"], c["G"], _cfg(c, exact=True))
     assert [r.sweeps, r.total_transforms, r.big_transforms, int(r.converged)] == list(c["counters"])
     assert np.array_equal(r.sigma, c["sigma"])
@@ -87,7 +81,7 @@ def _gpu_block(tw, cplx, cfg, epsn, grams):
 
 @pytest.mark.parametrize("tw", [2, 4, 8, 16, 32, 64])
 @pytest.mark.parametrize("cplx", [False, True])
-@pytest.mark.parametrize("variant", [0, 2, 4, 6])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 def test_inner_block_kernel_bitwise(tw, cplx, variant):
     cfg = hz.SolverConfig(variant_id=variant, block_width=tw // 2)
     epsn = EPS * np.sqrt(1024.0)
@@ -153,7 +147,6 @@ DMMA_CASES = [n for n in CASES if manifest()[n]["cfg"].get("block_width", 8) in 
 @pytest.mark.parametrize("name", DMMA_CASES)
 def test_dmma_mode_within_tolerance(name):
     c = load_case(name)
-    _skip_unsupported(c)
     n = c["n"]
     r = hz.solve(c["F"], c["G"], _cfg(c))
     # tolerances: sigma rel err <= 8 n eps vs the reference
