@@ -11,6 +11,7 @@
 // hzg_device.cuh), so given the same Grammians the factors, Z~ and the
 // counters are bitwise those of the reference's _block_task
 // (blocked.py:435-484; pointwise.py:161-293).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -495,13 +496,16 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   constexpr int NP = CPLX ? 2 : 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   auto& S = *reinterpret_cast<InnerSmem<TW, CPLX>*>(smem_raw);
-  const int pair = P.sp.p0 + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = blockDim.x;
   const KernelCfg& kc = P.kc;
 
   // ---- the inner strategy table ------------------------------------------
   for (int e = tid; e < P.isteps * TW; e += nt) S.tab[e] = (uint8_t)P.itable[e];
+
+  // a CTA may serve several pairs of the step (grid capped at launch)
+  for (int pair = P.sp.p0 + blockIdx.x; pair < P.sp.p0 + P.sp.pn; pair += gridDim.x) {
+  __syncthreads();  // the previous pair is done with shared memory
   if (tid == 0) {
     S.chol_fail[0] = S.chol_fail[1] = 0;
   }
@@ -967,6 +971,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
     cnt[2] = status;
     cnt[3] = sweeps;
   }
+  }  // pairs
 }
 
 template <int TW, bool CPLX, bool SWZ>
@@ -977,7 +982,15 @@ int launch_inner_g(const InnerParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(k_inner<TW, CPLX, SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_done = true;
   }
-  k_inner<TW, CPLX, SWZ><<<p.sp.pn, InnerGeo<TW, CPLX>::NW * 32, smem, s>>>(p);
+  // HZG_INNER_CTAS caps the CTAs of one launch (each then serves several
+  // pairs), leaving SM room for the streaming kernels of other groups
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = std::getenv("HZG_INNER_CTAS");
+    cap = e ? std::max(0, std::atoi(e)) : 0;
+  }
+  const int grid = cap > 0 && cap < p.sp.pn ? cap : p.sp.pn;
+  k_inner<TW, CPLX, SWZ><<<grid, InnerGeo<TW, CPLX>::NW * 32, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

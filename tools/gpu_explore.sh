@@ -1,5 +1,6 @@
 out=gpurun_out
 tag=${1:-x}
-python tools/phase_prof.py 4096 > $out/${tag}_phase.txt 2>&1
-HZG_LIB=scratch/nomath/libhzg_nomath.so python tools/phase_prof.py 4096 >> $out/${tag}_phase.txt 2>&1
-timeout 900 python tools/cmp_cond1024.py > $out/${tag}_cmp1024.txt 2>&1
+for g in 1 2 4 8 16; do
+  echo "groups $g" >> $out/${tag}_explore.txt
+  HZG_GROUPS=$g timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
+done
