@@ -1,6 +1,5 @@
 out=gpurun_out
 tag=${1:-x}
-for g in 1 2 4 8 16; do
-  echo "groups $g" >> $out/${tag}_explore.txt
-  HZG_GROUPS=$g timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
-done
+timeout 900 python -m pytest tests -m gpu -x -q > $out/${tag}_pytest.log 2>&1; echo "rc $?" >> $out/${tag}_pytest.log
+python tools/phase_prof.py 4096 > $out/${tag}_phase.txt 2>&1
+timeout 600 python tools/explore.py 4096 cond 16 fb 100 >> $out/${tag}_explore.txt 2>&1
