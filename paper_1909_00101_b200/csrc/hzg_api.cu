@@ -32,6 +32,18 @@ struct hzg_ctx {
   int64_t cstride = 0;      // doubles of compensated scratch per column / per thread (pow2 of the height)
   bool wavefront = false;   // schedule in circle-position order (ME)
   int groups = 1;           // position groups of the wavefront sweep graph
+  // fused postmultiply(k) + Grammian(k+1) along circle-position chains
+  bool fused = false;
+  int pg_L = 0, pg_nchains = 0, pg_maxexc = 0;
+  std::vector<int32_t> pg_chains_host;  // [osteps-1][nchains][L+1]
+  std::vector<int32_t> pg_links_host;   // [osteps-1][nchains][L+1][5]
+  std::vector<int32_t> pg_exc_host;     // [osteps-1][maxexc]
+  std::vector<int32_t> pg_nexc;         // [osteps-1]
+  std::vector<int32_t> all_pairs_host;  // 0 .. npairs-1
+  int32_t* d_pg_chains = nullptr;
+  int32_t* d_pg_links = nullptr;
+  int32_t* d_pg_exc = nullptr;
+  int32_t* d_all_pairs = nullptr;
   std::vector<cudaStream_t> gstreams;
   std::vector<cudaEvent_t> gevents;  // fork, joins[G], step events [2][G]
   std::vector<int32_t> colpair_host;  // [osteps][npairs][2]
@@ -165,21 +177,29 @@ int cuda_fail(hzg_ctx* c, cudaError_t e, const char* where) {
 
 // Grammian split geometry per matrix height (depends on m only, never on
 // the GPU count, so results are GPU-count invariant).
+// rows per Grammian split in DMMA mode (HZG_SPLIT_ROWS, for tuning)
+int64_t split_rows() {
+  const char* e = std::getenv("HZG_SPLIT_ROWS");
+  return e ? std::max<int64_t>(64, std::atoi(e)) / 64 * 64 : 512;
+}
+
 void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
+  const int64_t kSplitRows = split_rows();
   if (exact) {
     int64_t P = pow2c(m);
     chunk = std::max<int64_t>(32, std::min<int64_t>(P, 2048));
     nsplit = (int)std::max<int64_t>(1, P / chunk);
   } else {
-    // >= 512 rows per split CTA, at most 8 splits (partials stay a few
-    // percent of the Grammian's HBM reads); chunk a multiple of 64 rows
-    nsplit = (int)std::min<int64_t>(8, pow2c((m + 511) / 512));
+    // splits of at most 512 rows (a power-of-two count; the fused
+    // postmultiply + Grammian keeps a split's half tiles on chip), chunk a
+    // multiple of 64 rows.  Depends on m only, never on the GPU count.
+    nsplit = (int)pow2c((m + kSplitRows - 1) / kSplitRows);
     chunk = ((m + nsplit - 1) / nsplit + 63) / 64 * 64;
   }
 }
 
 struct Layout {
-  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, phase, comp, total;
+  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, phase, comp, pg, total;
 };
 
 Layout layout(const hzg_ctx* c) {
@@ -211,6 +231,8 @@ Layout layout(const hzg_ctx* c) {
   if (c->comp)
     cs = (size_t)c->cstride * 8 * std::max<size_t>((size_t)c->n, (size_t)c->npairs * 2 * 32);
   L.comp = take(cs);
+  L.pg = take((c->pg_chains_host.size() + c->pg_links_host.size() + c->pg_exc_host.size() +
+               c->all_pairs_host.size()) * 4);
   L.total = off;
   return L;
 }
@@ -291,6 +313,74 @@ int status_code(int64_t st) {
   return HZG_OK;
 }
 
+// Chains of circle positions for the fused postmultiply + Grammian (see
+// k_postgram): per step k < osteps-1, positions of one parity class in runs
+// of L+1 (p, p+2, ..., p+2L); link e joins positions e-1 and e when they
+// hold the two blocks of one pair of step k+1.  Next-step pairs no link
+// covers are listed as exceptions (their Grammian runs standalone after
+// the fused kernel).
+void build_postgram_tables(hzg_ctx* c) {
+  const int np = c->npairs, L = 16, w = c->w;
+  const int per_fam = (np + 1) / 2;
+  const int chains_per_fam = (per_fam + L) / (L + 1);
+  c->pg_L = L;
+  c->pg_nchains = 2 * chains_per_fam;
+  const int S = c->osteps - 1;
+  c->pg_chains_host.assign((size_t)S * c->pg_nchains * (L + 1), -1);
+  c->pg_links_host.assign((size_t)S * c->pg_nchains * (L + 1) * 5, -1);
+  c->pg_nexc.assign(S, 0);
+  std::vector<std::vector<int32_t>> exc(S);
+  std::vector<int> pos_of(c->nblk), half_of(c->nblk);
+  for (int k = 0; k < S; ++k) {
+    const int32_t* cur = &c->colpair_host[(size_t)k * np * 2];
+    const int32_t* nxt = &c->colpair_host[(size_t)(k + 1) * np * 2];
+    for (int i = 0; i < np; ++i)
+      for (int h = 0; h < 2; ++h) {
+        pos_of[cur[2 * i + h] / w] = i;
+        half_of[cur[2 * i + h] / w] = h;
+      }
+    // next pair j <- unordered source positions
+    std::vector<int> covered(np, 0);
+    auto find_next = [&](int pa, int pb) {
+      for (int j = std::max(0, std::min(pa, pb) - 2); j <= std::min(np - 1, std::max(pa, pb) + 2); ++j) {
+        const int s0 = pos_of[nxt[2 * j] / w], s1 = pos_of[nxt[2 * j + 1] / w];
+        if ((s0 == pa && s1 == pb) || (s0 == pb && s1 == pa)) return j;
+      }
+      return -1;
+    };
+    for (int fam = 0; fam < 2; ++fam)
+      for (int t = 0; t < chains_per_fam; ++t) {
+        const int ch = fam * chains_per_fam + t;
+        int32_t* el = &c->pg_chains_host[((size_t)k * c->pg_nchains + ch) * (L + 1)];
+        int32_t* lk = &c->pg_links_host[((size_t)k * c->pg_nchains + ch) * (L + 1) * 5];
+        for (int e = 0; e <= L; ++e) {
+          const int pos = fam + 2 * (t * (L + 1) + e);
+          if (pos >= np) break;
+          el[e] = pos;
+          if (e == 0) continue;
+          const int j = find_next(el[e - 1], pos);
+          if (j < 0 || covered[j]) continue;
+          covered[j] = 1;
+          const int b0 = nxt[2 * j] / w, b1 = nxt[2 * j + 1] / w;
+          lk[e * 5 + 0] = j;
+          lk[e * 5 + 1] = pos_of[b0] == pos ? 1 : 0;
+          lk[e * 5 + 2] = half_of[b0];
+          lk[e * 5 + 3] = pos_of[b1] == pos ? 1 : 0;
+          lk[e * 5 + 4] = half_of[b1];
+        }
+      }
+    for (int j = 0; j < np; ++j)
+      if (!covered[j]) exc[k].push_back(j);
+    c->pg_nexc[k] = (int)exc[k].size();
+    c->pg_maxexc = std::max(c->pg_maxexc, c->pg_nexc[k]);
+  }
+  c->pg_exc_host.assign((size_t)S * std::max(1, c->pg_maxexc), 0);
+  for (int k = 0; k < S; ++k)
+    for (size_t q = 0; q < exc[k].size(); ++q) c->pg_exc_host[(size_t)k * std::max(1, c->pg_maxexc) + q] = exc[k][q];
+  c->all_pairs_host.resize(np);
+  for (int i = 0; i < np; ++i) c->all_pairs_host[i] = i;
+}
+
 }  // namespace
 
 extern "C" {
@@ -349,6 +439,17 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
     c->gw.chunk[1] = mG;
   }
   c->gw.smax = std::max(c->gw.nsplit[0], c->gw.nsplit[1]);
+  // fused postmultiply + Grammian: DMMA mode, real, w = 16, the ME circle
+  // schedule of a single rank, splits of at most 256 rows.  Opt-in
+  // (HZG_FUSED=1 with HZG_SPLIT_ROWS=256): bitwise equal to the separate
+  // kernels, but measured slower on B200 so far (profiles/r01_fused.txt)
+  {
+    const char* env = std::getenv("HZG_FUSED");
+    const bool want = env && std::atoi(env) != 0;
+    c->fused = want && c->use_dmma && !c->comp && !cfg->shorten_qr && c->wavefront &&
+               postgram_supported(w, c->cplx) && c->osteps >= 2 && c->gw.chunk[0] <= 256 && c->gw.chunk[1] <= 256;
+    if (c->fused) build_postgram_tables(c);
+  }
 
   // QR scratch slots: one per pair when every pair is shortened by QR,
   // otherwise a few shared by the rare Cholesky failures
@@ -366,6 +467,11 @@ int hzg_set_schedule(hzg_ctx* c, const int32_t* colpairs, int32_t osteps, int32_
   c->npairs = npairs;
   c->colpair_host.assign(colpairs, colpairs + (size_t)osteps * npairs * 2);
   c->wavefront = false;
+  c->fused = false;
+  c->pg_chains_host.clear();
+  c->pg_links_host.clear();
+  c->pg_exc_host.clear();
+  c->all_pairs_host.clear();
   c->qr_slots = c->cfg.shorten_qr ? npairs : std::max(1, std::min(16, npairs));
   return HZG_OK;
 }
@@ -403,6 +509,21 @@ int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double*
   if ((e = cudaMemcpyAsync(c->d_itable, c->itable_host.data(), c->itable_host.size() * 4, cudaMemcpyHostToDevice,
                            c->stream)) != cudaSuccess)
     return cuda_fail(c, e, "upload inner table");
+  if (c->fused) {
+    int32_t* base = (int32_t*)(c->ws + L.pg);
+    c->d_pg_chains = base;
+    c->d_pg_links = c->d_pg_chains + c->pg_chains_host.size();
+    c->d_pg_exc = c->d_pg_links + c->pg_links_host.size();
+    c->d_all_pairs = c->d_pg_exc + c->pg_exc_host.size();
+    cudaMemcpyAsync(c->d_pg_chains, c->pg_chains_host.data(), c->pg_chains_host.size() * 4, cudaMemcpyHostToDevice,
+                    c->stream);
+    cudaMemcpyAsync(c->d_pg_links, c->pg_links_host.data(), c->pg_links_host.size() * 4, cudaMemcpyHostToDevice,
+                    c->stream);
+    cudaMemcpyAsync(c->d_pg_exc, c->pg_exc_host.data(), c->pg_exc_host.size() * 4, cudaMemcpyHostToDevice,
+                    c->stream);
+    cudaMemcpyAsync(c->d_all_pairs, c->all_pairs_host.data(), c->all_pairs_host.size() * 4, cudaMemcpyHostToDevice,
+                    c->stream);
+  }
   cudaMemsetAsync(c->d_qrlock, 0, (size_t)c->qr_slots * 4, c->stream);
   cudaMemsetAsync(c->io.counts, 0, (size_t)c->osteps * c->npairs * 16, c->stream);
   if (!c->h_ctr) {
@@ -487,9 +608,35 @@ static int build_graph(hzg_ctx* c) {
   if ((e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
     return cuda_fail(c, e, "begin capture");
   int rc = HZG_OK;
+  if (c->fused) {
+    // step 0's Grammian, then per step: inner -> fused postmultiply of F, G
+    // with the next step's Grammian partials, postmultiply of Z, Grammian of
+    // the next-step pairs no chain link covers
+    cudaStream_t s = c->cap;
+    StepPairs all{c->d_colpair, c->npairs, 0, c->npairs};
+    KernelCfg kc = kernel_cfg(c);
+    rc = launch_gram_dmma(c->F, c->G, all, 0, c->w, c->cplx, c->gw, s);
+    for (int st = 0; st < c->osteps && rc == HZG_OK; ++st) {
+      rc = launch_inner(c->F, c->G, all, st, kc, c->gw, c->d_itable, c->isteps, c->io, c->d_qr, c->qr_slots,
+                        c->d_qrlock, s);
+      if (rc) break;
+      if (st + 1 < c->osteps) {
+        const size_t L1 = (size_t)c->pg_L + 1;
+        PostGramTables tb{c->d_pg_chains + (size_t)st * c->pg_nchains * L1,
+                          c->d_pg_links + (size_t)st * c->pg_nchains * L1 * 5, c->pg_nchains, c->pg_L};
+        rc = launch_postgram(c->F, c->G, all, st, c->w, c->cplx, c->io, c->gw, tb, s);
+        if (!rc) rc = launch_postmult_dmma(c->F, c->G, c->Z, all, st, c->w, c->cplx, c->io, s, 2, 1);
+        if (!rc && c->pg_nexc[st] > 0)
+          rc = launch_gram_dmma(c->F, c->G, all, st + 1, c->w, c->cplx, c->gw, s,
+                                c->d_pg_exc + (size_t)st * std::max(1, c->pg_maxexc), c->pg_nexc[st]);
+      } else {
+        rc = launch_postmult_dmma(c->F, c->G, c->Z, all, st, c->w, c->cplx, c->io, s);
+      }
+    }
+  }
   cudaEventRecord(fork, c->cap);
   for (int g = 0; g < G; ++g) cudaStreamWaitEvent(c->gstreams[g], fork, 0);
-  for (int st = 0; st < c->osteps && rc == HZG_OK; ++st) {
+  for (int st = 0; st < c->osteps && rc == HZG_OK && !c->fused; ++st) {
     for (int g = 0; g < G && rc == HZG_OK; ++g) {
       cudaStream_t s = c->gstreams[g];
       if (st > 0) {
@@ -742,6 +889,11 @@ int hzg_launch_counts(const hzg_ctx* c, int64_t* per_sweep, int64_t* per_solve_f
   const int G = c->gexec ? c->groups : choose_groups(c);
   // sweep graph: 3 step kernels per (step, group), counter fold, rescale
   if (per_sweep) *per_sweep = (int64_t)c->osteps * G * 3 + 2;
+  if (per_sweep && c->fused) {
+    int64_t n = 1 + 2 + (int64_t)c->osteps * 1 + (int64_t)(c->osteps - 1) * 2 + 1;  // gram0, counters, rescale, inner, postgram+postZ, last post
+    for (int k = 0; k + 1 < c->osteps; ++k) n += c->pg_nexc[k] > 0 ? 1 : 0;
+    *per_sweep = n;
+  }
   // k_prescale; final k_rescale, k_keep, k_keep_count, k_rank, k_gather
   if (per_solve_fixed) *per_solve_fixed = 6;
   return HZG_OK;

@@ -62,6 +62,7 @@ struct GramParams {
   StepPairs sp;
   int step;
   GramWS gw;
+  const int32_t* plist;  // optional: the pairs of this launch (blockIdx.x indexes it)
 };
 
 template <int TW, bool CPLX>
@@ -73,7 +74,8 @@ __global__ void __launch_bounds__(GramCfg<TW, CPLX>::NWARP * 32) k_gram_dmma(Gra
   double* stages = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::NS * C::STAGE * sizeof(double));
 
-  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
+  const int pair = P.plist ? P.plist[blockIdx.x] : P.sp.p0 + blockIdx.x;
+  const int mat = blockIdx.y, split = blockIdx.z;
   if (split >= P.gw.nsplit[mat]) return;
   const Plane& Y = P.Y[mat];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -190,130 +192,6 @@ __global__ void __launch_bounds__(GramCfg<TW, CPLX>::NWARP * 32) k_gram_dmma(Gra
 }
 
 // ---------------------------------------------------------------------------
-// Grammian partials, k-split form (2w <= 32).  Every warp keeps all upper
-// 8x8 tiles in registers and takes an interleaved quarter of the k-steps of
-// each 64-row tile (complex: warps 0-1 the real plane, 2-3 the imaginary
-// plane, each half of the k-steps), so the DMMA work is split evenly over the
-// four SM sub-partitions; the per-warp partial sums are folded in a fixed
-// order through shared memory at the end.
-// ---------------------------------------------------------------------------
-template <int TW, bool CPLX>
-struct GramKsCfg {
-  static constexpr int NT = TW / 8;
-  static constexpr int NTILE = NT * (NT + 1) / 2;
-  static constexpr int NWARP = 4;
-  static constexpr int NP = CPLX ? 2 : 1;
-  static constexpr int NS = 3;
-  static constexpr int KSTRIDE = CPLX ? 2 : 4;  // warps sharing one plane's k-steps
-  static constexpr size_t STAGE = (size_t)NP * TW * kRS;
-  static constexpr size_t RED = (size_t)NWARP * NTILE * 64;  // doubles
-  static constexpr size_t BUF = NS * STAGE > RED ? NS * STAGE : RED;
-  static constexpr size_t SMEM = BUF * sizeof(double) + 64;
-};
-
-template <int TW, bool CPLX>
-__global__ void __launch_bounds__(128) k_gram_ks(GramParams P) {
-  using C = GramKsCfg<TW, CPLX>;
-  constexpr int NP = C::NP, NT = C::NT, NTILE = C::NTILE;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* stages = reinterpret_cast<double*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BUF * sizeof(double));
-
-  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
-  if (split >= P.gw.nsplit[mat]) return;
-  const Plane& Y = P.Y[mat];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int plane = CPLX ? (warp >> 1) : 0;
-  const int ks0 = CPLX ? (warp & 1) : warp;
-  const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
-  const int64_t L = P.gw.chunk[mat];
-  const int64_t rbeg = (int64_t)split * L;
-  const int64_t rend = rbeg + L < Y.rows ? rbeg + L : Y.rows;
-  const int ntiles = rend > rbeg ? (int)((rend - rbeg + kR - 1) / kR) : 0;
-
-  if (tid == 0) {
-    for (int q = 0; q < C::NS; ++q) mbar_init(&full[q], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0)
-    for (int q = 0; q < C::NS && q < ntiles; ++q) {
-      int64_t r0 = rbeg + (int64_t)q * kR;
-      int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
-      issue_tile_load<TW, NP>(Y, cp, r0, nv, stages + q * C::STAGE, &full[q], lane);
-    }
-
-  double acc[NTILE][2];
-#pragma unroll
-  for (int q = 0; q < NTILE; ++q) acc[q][0] = acc[q][1] = 0.0;
-
-  for (int it = 0; it < ntiles; ++it) {
-    const int s = it % C::NS;
-    mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
-    const double* st = stages + s * C::STAGE;
-    const int64_t r0 = rbeg + (int64_t)it * kR;
-    const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
-#pragma unroll
-    for (int ks = ks0; ks < kR / 4; ks += C::KSTRIDE) {
-      const int k = ks * 4 + t;
-      const bool ok = k < nv;
-      double fr[NT], fi[NT];
-#pragma unroll
-      for (int cg = 0; cg < NT; ++cg) {
-        fr[cg] = ok ? st[(size_t)(cg * 8 + g) * kRS + k] : 0.0;
-        fi[cg] = (CPLX && ok) ? st[(size_t)(TW + cg * 8 + g) * kRS + k] : 0.0;
-      }
-      int q = 0;
-#pragma unroll
-      for (int I = 0; I < NT; ++I)
-#pragma unroll
-        for (int J = I; J < NT; ++J, ++q) {
-          if (!CPLX) {
-            dmma884(acc[q][0], acc[q][1], fr[I], fr[J]);
-          } else if (plane == 0) {  // Re = ar br + ai bi
-            dmma884(acc[q][0], acc[q][1], fr[I], fr[J]);
-            dmma884(acc[q][0], acc[q][1], fi[I], fi[J]);
-          } else {  // Im = ar bi - ai br
-            dmma884(acc[q][0], acc[q][1], fr[I], fi[J]);
-            dmma884(acc[q][0], acc[q][1], -fi[I], fr[J]);
-          }
-        }
-    }
-    __syncthreads();
-    if (warp == 0 && it + C::NS < ntiles) {
-      int64_t r1 = rbeg + (int64_t)(it + C::NS) * kR;
-      int nv1 = (int)(rend - r1 < kR ? rend - r1 : kR);
-      issue_tile_load<TW, NP>(Y, cp, r1, nv1, stages + s * C::STAGE, &full[s], lane);
-    }
-  }
-  // fold the per-warp partials in a fixed order
-  double* red = stages;  // all bulk loads have landed and been consumed
-#pragma unroll
-  for (int q = 0; q < NTILE; ++q) {
-    red[((size_t)warp * NTILE + q) * 64 + lane * 2] = acc[q][0];
-    red[((size_t)warp * NTILE + q) * 64 + lane * 2 + 1] = acc[q][1];
-  }
-  __syncthreads();
-  double* out = P.gw.part + (((int64_t)pair * 2 + mat) * P.gw.smax + split) * NP * TW * TW;
-  for (int e = tid; e < NP * NTILE * 64; e += blockDim.x) {
-    const int pl = e / (NTILE * 64), rem = e % (NTILE * 64), q = rem / 64, l = (rem % 64) / 2, h = rem % 2;
-    double v = 0.0;
-#pragma unroll
-    for (int wv = 0; wv < C::KSTRIDE; ++wv) v += red[((size_t)(pl * C::KSTRIDE + wv) * NTILE + q) * 64 + l * 2 + h];
-    // tile q -> (I, J)
-    int I = 0, qq = q;
-    while (qq >= NT - I) {
-      qq -= NT - I;
-      ++I;
-    }
-    const int J = I + qq;
-    const int r = I * 8 + (l >> 2), c = J * 8 + 2 * (l & 3) + h;
-    out[(size_t)pl * TW * TW + (size_t)c * TW + r] = v;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Postmultiply [Y_p Y_q] <- [Y_p Y_q] Z~ for F, G and Z.  4 warps along the
 // 64 rows (16 rows each) x WN warps along the columns (32 columns each).
 // ---------------------------------------------------------------------------
@@ -336,6 +214,7 @@ struct PostParams {
   int step;
   InnerOut io;
   int64_t chunk;  // rows per CTA
+  int mat0;       // first matrix of the launch (blockIdx.y + mat0: 0 F, 1 G, 2 Z)
 };
 
 template <int TW, bool CPLX>
@@ -343,7 +222,7 @@ __global__ void __launch_bounds__(PostCfg<TW, CPLX>::NWARP * 32) k_post_dmma(Pos
   using C = PostCfg<TW, CPLX>;
   constexpr int NP = C::NP;
   constexpr int w = TW / 2;
-  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y;
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y + P.mat0;
   if (P.io.ident[pair]) return;
   const Plane& Y = P.Y[mat];
   const int64_t rbeg = (int64_t)blockIdx.z * P.chunk;
@@ -489,7 +368,8 @@ __global__ void __launch_bounds__(160) k_gram_ws(GramParams P) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::BUF * sizeof(double));
   uint64_t* empty = full + C::NS;
 
-  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y, split = blockIdx.z;
+  const int pair = P.plist ? P.plist[blockIdx.x] : P.sp.p0 + blockIdx.x;
+  const int mat = blockIdx.y, split = blockIdx.z;
   if (split >= P.gw.nsplit[mat]) return;
   const Plane& Y = P.Y[mat];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -598,7 +478,7 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
   using C = PostWsCfg<TW, CPLX>;
   constexpr int NP = C::NP;
   constexpr int w = TW / 2;
-  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y;
+  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y + P.mat0;
   if (P.io.ident[pair]) return;
   const Plane& Y = P.Y[mat];
   const int64_t rbeg = (int64_t)blockIdx.z * P.chunk;
@@ -716,6 +596,230 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused postmultiply (step k) + Grammian partials (step k + 1), 2w = 32 real.
+//
+// Pair i of step k + 1 takes one block from pair i - 1 and one from pair
+// i + 1 of step k (circle positions), so walking the positions of one
+// parity class in order, every two consecutive pairs hold the two blocks of
+// one next-step pair.  A CTA owns one row split of F or G and a chain of
+// positions p, p + 2, ..., p + 2L: for each position it streams the pair's
+// row tiles through TMA, applies Z~ with DMMA (identical to k_post_ws) and
+// stores them back, and -- while the tile is in shared memory -- adds the
+// tile's contribution to the Grammian of the next-step pair formed with the
+// previous position, whose needed half tile it kept (the carry).  The
+// Grammian arithmetic is that of k_gram_ws over the same split rows, so
+// the partials are bitwise those of the unfused path.  F and G are read
+// once and written once per step instead of read twice.
+// ---------------------------------------------------------------------------
+struct PGCfg {
+  static constexpr int TW = 32, W = 16;
+  static constexpr int NS = 2;
+  static constexpr int NT = TW / 8;
+  static constexpr int NTILE = NT * (NT + 1) / 2;
+  static constexpr int ZS = TW + 4;
+  static constexpr int MAXT = 4;  // row tiles per split (split <= 256 rows)
+  static constexpr size_t STAGE = (size_t)TW * kRS;
+  static constexpr size_t CARRY = (size_t)MAXT * W * kRS;
+  static constexpr size_t RED = (size_t)4 * NTILE * 64;
+  static constexpr size_t SMEM = (NS * STAGE + CARRY + (size_t)TW * ZS + RED) * sizeof(double) + 2 * NS * 8 + 64;
+};
+
+struct PostGramParams {
+  Plane Y[2];
+  StepPairs sp;  // the current step's pairs (colpair of `step`)
+  int step;
+  InnerOut io;
+  GramWS gw;
+  PostGramTables t;
+};
+
+__global__ void __launch_bounds__(160) k_postgram(PostGramParams P) {
+  using C = PGCfg;
+  constexpr int TW = C::TW, W = C::W, NT = C::NT, NTILE = C::NTILE;
+  const int chain = blockIdx.x, split = blockIdx.y, mat = blockIdx.z;
+  if (split >= P.gw.nsplit[mat]) return;
+  const Plane& Y = P.Y[mat];
+  const int64_t L = P.gw.chunk[mat];
+  const int64_t rbeg = (int64_t)split * L;
+  const int64_t rend = rbeg + L < Y.rows ? rbeg + L : Y.rows;
+  if (rend <= rbeg) return;
+  const int ntiles = (int)((rend - rbeg + kR - 1) / kR);
+  const int32_t* elems = P.t.chains + (int64_t)chain * (P.t.L + 1);
+  const int32_t* links = P.t.links + (int64_t)chain * (P.t.L + 1) * 5;
+  int nel = 0;
+  while (nel <= P.t.L && elems[nel] >= 0) ++nel;
+  const int total = nel * ntiles;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* stages = reinterpret_cast<double*>(smem_raw);
+  double* carry = stages + C::NS * C::STAGE;
+  double* zs = carry + C::CARRY;
+  double* red = zs + (size_t)TW * C::ZS;
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + C::RED);
+  uint64_t* done = full + C::NS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int q = 0; q < C::NS; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&done[q], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 4) {  // producer: tile loads, and stores of transformed tiles
+    auto store_tile = [&](int it) {
+      const int s = it % C::NS;
+      mbar_wait(&done[s], (uint32_t)((it / C::NS) & 1));
+      const int pair = elems[it / ntiles];
+      if (P.io.ident[pair]) return;  // Z~ = I: the tile is unchanged
+      const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
+      const int64_t r0 = rbeg + (int64_t)(it % ntiles) * kR;
+      const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+      bulk_s2g(Y.re + pair_col(cp, W, lane) * Y.ld + r0, stages + s * C::STAGE + (size_t)lane * kRS,
+               (uint32_t)nv * 8u);
+      bulk_commit();
+    };
+    for (int it = 0; it < total; ++it) {
+      const int s = it % C::NS;
+      if (it >= C::NS) {
+        store_tile(it - C::NS);
+        bulk_wait_read<0>();
+        __syncwarp();
+      }
+      const int pair = elems[it / ntiles];
+      const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
+      const int64_t r0 = rbeg + (int64_t)(it % ntiles) * kR;
+      const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+      issue_tile_load<TW, 1>(Y, cp, r0, nv, stages + s * C::STAGE, &full[s], lane);
+    }
+    for (int it = total > C::NS ? total - C::NS : 0; it < total; ++it) store_tile(it);
+    bulk_wait_all<0>();
+    return;
+  }
+
+  const int g = lane >> 2, t = lane & 3;
+  double acc[NTILE][2];
+  for (int e = 0; e < nel; ++e) {
+    const int pair = elems[e];
+    const bool ident = P.io.ident[pair] != 0;
+    // Z~ of this position (column-major, padded)
+    if (!ident) {
+      const double* zsrc = P.io.zt + (int64_t)pair * TW * TW;
+      for (int q = tid; q < TW * TW; q += 128) zs[(q / TW) * C::ZS + q % TW] = zsrc[q];
+    }
+    // link e: the next-step pair made of (position e-1, position e)
+    const int* lk = links + e * 5;
+    const int jn = e >= 1 ? lk[0] : -1;
+    // the half of this position the next link needs, kept in the carry
+    const int* lk1 = links + (e + 1) * 5;
+    const int hcarry = (e + 1 < nel && lk1[0] >= 0) ? (lk1[1] == 0 ? lk1[2] : lk1[4]) : -1;
+#pragma unroll
+    for (int q = 0; q < NTILE; ++q) acc[q][0] = acc[q][1] = 0.0;
+    consumer_bar();
+    for (int tt = 0; tt < ntiles; ++tt) {
+      const int it = e * ntiles + tt;
+      const int s = it % C::NS;
+      mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
+      double* st = stages + s * C::STAGE;
+      const int64_t r0 = rbeg + (int64_t)tt * kR;
+      const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+      if (!ident) {  // postmultiply this warp's 16 rows (k_post_ws, real)
+        double pacc[2][NT][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) pacc[mi][ni][0] = pacc[mi][ni][1] = 0.0;
+#pragma unroll 2
+        for (int ks = 0; ks < TW / 4; ++ks) {
+          const int k = ks * 4 + t;
+          double ar[2];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) ar[mi] = st[(size_t)k * kRS + warp * 16 + mi * 8 + g];
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const double zr = zs[(size_t)(ni * 8 + g) * C::ZS + k];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) dmma884(pacc[mi][ni][0], pacc[mi][ni][1], ar[mi], zr);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const int row = warp * 16 + mi * 8 + g;
+            const int col = ni * 8 + 2 * t;
+            st[(size_t)col * kRS + row] = pacc[mi][ni][0];
+            st[(size_t)(col + 1) * kRS + row] = pacc[mi][ni][1];
+          }
+      }
+      consumer_bar();  // the transformed tile is complete
+      if (jn >= 0) {   // Grammian contribution of this tile (k_gram_ws, real)
+        const double* cbase = carry + (size_t)tt * W * kRS;
+        const double* colp[NT];
+#pragma unroll
+        for (int cg = 0; cg < NT; ++cg) {
+          const int c = cg * 8 + g;              // next-pair column
+          const int src = c < W ? 1 : 3;         // (elem, half) of its block
+          const int cw = c % W;
+          colp[cg] = lk[src] == 0 ? cbase + (size_t)cw * kRS : st + (size_t)(lk[src + 1] * W + cw) * kRS;
+        }
+#pragma unroll
+        for (int ks = warp; ks < kR / 4; ks += 4) {
+          const int k = ks * 4 + t;
+          const bool ok = k < nv;
+          double fr[NT];
+#pragma unroll
+          for (int cg = 0; cg < NT; ++cg) fr[cg] = ok ? colp[cg][k] : 0.0;
+          int q = 0;
+#pragma unroll
+          for (int I = 0; I < NT; ++I)
+#pragma unroll
+            for (int J = I; J < NT; ++J, ++q) dmma884(acc[q][0], acc[q][1], fr[I], fr[J]);
+        }
+      }
+      consumer_bar();  // carry and tile reads done
+      if (hcarry >= 0) {
+        double* cdst = carry + (size_t)tt * W * kRS;
+        for (int q = tid; q < W * kR; q += 128) {
+          const int c = q / kR, r = q % kR;
+          cdst[(size_t)c * kRS + r] = st[(size_t)(hcarry * W + c) * kRS + r];
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[s]);
+    }
+    if (jn >= 0) {  // fold the warps' partials in k_gram_ws's fixed order
+#pragma unroll
+      for (int q = 0; q < NTILE; ++q) {
+        red[((size_t)warp * NTILE + q) * 64 + lane * 2] = acc[q][0];
+        red[((size_t)warp * NTILE + q) * 64 + lane * 2 + 1] = acc[q][1];
+      }
+      consumer_bar();
+      double* out = P.gw.part + (((int64_t)jn * 2 + mat) * P.gw.smax + split) * TW * TW;
+      for (int q2 = tid; q2 < NTILE * 64; q2 += 128) {
+        const int q = q2 / 64, l = (q2 % 64) / 2, h = q2 % 2;
+        double v = 0.0;
+#pragma unroll
+        for (int wv = 0; wv < 4; ++wv) v += red[((size_t)wv * NTILE + q) * 64 + l * 2 + h];
+        int I = 0, qq = q;
+        while (qq >= NT - I) {
+          qq -= NT - I;
+          ++I;
+        }
+        const int J = I + qq;
+        const int r = I * 8 + (l >> 2), c = J * 8 + 2 * (l & 3) + h;
+        out[(size_t)c * TW + r] = v;
+      }
+    }
+    consumer_bar();  // Z~ and the fold buffer are free again
+  }
+}
+
 template <typename K>
 void set_smem(K k, size_t bytes) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -735,19 +839,6 @@ int gram_t(const GramParams& p, cudaStream_t s) {
 }
 
 template <int TW, bool CPLX>
-int gram_ks_t(const GramParams& p, cudaStream_t s) {
-  using C = GramKsCfg<TW, CPLX>;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_gram_ks<TW, CPLX>, C::SMEM);
-    once = true;
-  }
-  dim3 grid(p.sp.pn, 2, p.gw.smax);
-  k_gram_ks<TW, CPLX><<<grid, 128, C::SMEM, s>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
-}
-
-template <int TW, bool CPLX>
 int gram_ws_t(const GramParams& p, cudaStream_t s) {
   using C = GramWsCfg<TW, CPLX>;
   static bool once = false;
@@ -761,27 +852,27 @@ int gram_ws_t(const GramParams& p, cudaStream_t s) {
 }
 
 template <int TW, bool CPLX>
-int post_ws_t(const PostParams& p, int64_t mmax, cudaStream_t s) {
+int post_ws_t(const PostParams& p, int64_t mmax, int nmats, cudaStream_t s) {
   using C = PostWsCfg<TW, CPLX>;
   static bool once = false;
   if (!once) {
     set_smem(k_post_ws<TW, CPLX>, C::SMEM);
     once = true;
   }
-  dim3 grid(p.sp.pn, 3, (unsigned)((mmax + p.chunk - 1) / p.chunk));
+  dim3 grid(p.sp.pn, nmats, (unsigned)((mmax + p.chunk - 1) / p.chunk));
   k_post_ws<TW, CPLX><<<grid, 160, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 template <int TW, bool CPLX>
-int post_t(const PostParams& p, int64_t mmax, cudaStream_t s) {
+int post_t(const PostParams& p, int64_t mmax, int nmats, cudaStream_t s) {
   using C = PostCfg<TW, CPLX>;
   static bool once = false;
   if (!once) {
     set_smem(k_post_dmma<TW, CPLX>, C::SMEM);
     once = true;
   }
-  dim3 grid(p.sp.pn, 3, (unsigned)((mmax + p.chunk - 1) / p.chunk));
+  dim3 grid(p.sp.pn, nmats, (unsigned)((mmax + p.chunk - 1) / p.chunk));
   k_post_dmma<TW, CPLX><<<grid, C::NWARP * 32, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
@@ -790,9 +881,29 @@ int post_t(const PostParams& p, int64_t mmax, cudaStream_t s) {
 
 bool dmma_supported(int w) { return w == 8 || w == 16 || w == 32; }
 
+bool postgram_supported(int w, int cplx) { return w == 16 && !cplx; }
+
+int launch_postgram(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
+                    const InnerOut& io, const GramWS& gw, const PostGramTables& t, cudaStream_t s) {
+  if (!postgram_supported(w, cplx)) return 4;
+  static bool once = false;
+  if (!once) {
+    set_smem(k_postgram, PGCfg::SMEM);
+    once = true;
+  }
+  PostGramParams p{{F, G}, sp, step, io, gw, t};
+  dim3 grid(t.nchains, gw.smax, 2);
+  k_postgram<<<grid, 160, PGCfg::SMEM, s>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 int launch_gram_dmma(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
-                     const GramWS& gw, cudaStream_t s) {
-  GramParams p{{F, G}, sp, step, gw};
+                     const GramWS& gw, cudaStream_t s, const int32_t* plist, int npl) {
+  GramParams p{{F, G}, sp, step, gw, plist};
+  if (plist) {  // an explicit pair list: blockIdx.x indexes it
+    if (npl <= 0) return 0;
+    p.sp.pn = npl;
+  }
   switch (2 * w) {
     case 16:
       return cplx ? gram_ws_t<16, true>(p, s) : gram_ws_t<16, false>(p, s);
@@ -805,18 +916,19 @@ int launch_gram_dmma(const Plane& F, const Plane& G, const StepPairs& sp, int st
 }
 
 int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const StepPairs& sp, int step, int w,
-                         int cplx, const InnerOut& io, cudaStream_t s) {
-  int64_t mmax = F.rows > G.rows ? F.rows : G.rows;
-  if (Z.rows > mmax) mmax = Z.rows;
-  PostParams p{{F, G, Z}, sp, step, io, 1024};
+                         int cplx, const InnerOut& io, cudaStream_t s, int mat0, int nmats) {
+  int64_t mmax = 0;
+  const Plane* Y[3] = {&F, &G, &Z};
+  for (int q = mat0; q < mat0 + nmats; ++q) mmax = Y[q]->rows > mmax ? Y[q]->rows : mmax;
+  PostParams p{{F, G, Z}, sp, step, io, 1024, mat0};
   switch (2 * w) {
     case 16:
-      return cplx ? post_ws_t<16, true>(p, mmax, s) : post_ws_t<16, false>(p, mmax, s);
+      return cplx ? post_ws_t<16, true>(p, mmax, nmats, s) : post_ws_t<16, false>(p, mmax, nmats, s);
     case 32:
-      return cplx ? post_ws_t<32, true>(p, mmax, s) : post_ws_t<32, false>(p, mmax, s);
+      return cplx ? post_ws_t<32, true>(p, mmax, nmats, s) : post_ws_t<32, false>(p, mmax, nmats, s);
     case 64:
       p.chunk = 512;
-      return cplx ? post_t<64, true>(p, mmax, s) : post_t<64, false>(p, mmax, s);
+      return cplx ? post_t<64, true>(p, mmax, nmats, s) : post_t<64, false>(p, mmax, nmats, s);
   }
   return 4;
 }

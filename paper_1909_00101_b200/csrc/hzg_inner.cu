@@ -79,6 +79,7 @@ __device__ __forceinline__ double fold_splits(const double* p, int64_t stride, i
     case 8: return split_tree<8>(p, stride);
     case 16: return split_tree<16>(p, stride);
     case 32: return split_tree<32>(p, stride);
+    case 64: return split_tree<64>(p, stride);
     default: {
       PairwiseAcc<16> acc;
       acc.reset();

@@ -73,15 +73,28 @@ int launch_gram_comp(const Plane& F, const Plane& G, const StepPairs& sp, int st
                      const GramWS& gw, double* scratch, int64_t pstride, cudaStream_t s);
 int launch_gram_exact(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
                       const GramWS& gw, cudaStream_t s);
+// plist (optional): explicit pairs of the launch (npl of them) instead of sp's range
 int launch_gram_dmma(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
-                     const GramWS& gw, cudaStream_t s);
+                     const GramWS& gw, cudaStream_t s, const int32_t* plist = nullptr, int npl = 0);
 int launch_inner(const Plane& F, const Plane& G, const StepPairs& sp, int step, const KernelCfg& kc,
                  const GramWS& gw, const int32_t* itable, int isteps, const InnerOut& io, double* qr_scratch,
                  int qr_slots, int32_t* qr_slot_ctr, cudaStream_t s);
 int launch_postmult_exact(const Plane& F, const Plane& G, const Plane& Z, const StepPairs& sp, int step, int w,
                           int cplx, const InnerOut& io, cudaStream_t s);
+// matrices [mat0, mat0 + nmats) of {F, G, Z}
 int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const StepPairs& sp, int step, int w,
-                         int cplx, const InnerOut& io, cudaStream_t s);
+                         int cplx, const InnerOut& io, cudaStream_t s, int mat0 = 0, int nmats = 3);
+
+// Fused postmultiply of step `step` (F and G) and Grammian partials of step
+// `step + 1` along chains of circle positions (hzg_dmma.cu, 2w = 32, real).
+struct PostGramTables {
+  const int32_t* chains;  // [nchains][L + 1] current positions, -1 padded
+  const int32_t* links;   // [nchains][L + 1][5]: next pair, src of its first block (elem, half), of its second
+  int nchains, L;
+};
+int launch_postgram(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
+                    const InnerOut& io, const GramWS& gw, const PostGramTables& t, cudaStream_t s);
+bool postgram_supported(int w, int cplx);
 int launch_counters(const int32_t* counts, int64_t nentries, int64_t* out, cudaStream_t s);
 int launch_finalize(const Plane& U, const Plane& V, const Plane& Z, int64_t n, int64_t n0, int64_t mF0, int64_t mG0,
                     int cplx, int sort, const double* sigF, const double* sigG, const double* sig, Plane Uo, Plane Vo,

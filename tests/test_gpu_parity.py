@@ -292,3 +292,38 @@ def test_block_partitioned_1024_eight_ranks():
     r = hz.solve(F, G, cfg, workers=8)
     assert r.workers == 8
     assert np.array_equal(r.sigma, one.sigma) and np.array_equal(r.Z.re, one.Z.re)
+
+
+@pytest.mark.parametrize("name", ["genpair256_w16", "gauss200_w16", "corpus64_real_w16", "gauss1024"])
+def test_fused_postgram_bitwise_equals_unfused(name, monkeypatch):
+    """The fused postmultiply(k) + Grammian(k+1) kernel (k_postgram) must give
+    bitwise the same solve as the separate Grammian / postmultiply kernels:
+    same split geometry, same DMMA accumulation order."""
+    if name == "gauss1024":
+        g = O.gaussian_stream(77, 2 * 1024 * 1024)
+        F = g[: 1024 * 1024].reshape((1024, 1024), order="F")
+        G = g[1024 * 1024:].reshape((1024, 1024), order="F")
+        cfg = hz.SolverConfig(block_width=16)
+    else:
+        c = load_case(name)
+        F, G, cfg = c["F"], c["G"], _cfg(c)
+    monkeypatch.setenv("HZG_FUSED", "1")  # the fused path needs splits of <= 256 rows
+    monkeypatch.setenv("HZG_SPLIT_ROWS", "256")
+
+    def launches():
+        p = hz.MatrixPlanePair.from_dense(F)
+        q = hz.MatrixPlanePair.from_dense(G)
+        planes, _, _, _ = hz.upload_bordered(p, q, cfg.block_width)
+        d = hz.DeviceGsvd(planes, cfg)
+        n = d.launch_counts()[0]
+        d.close()
+        return n
+
+    fused_launches = launches()
+    a = hz.solve(F, G, cfg)
+    monkeypatch.setenv("HZG_FUSED", "0")
+    assert launches() != fused_launches  # the fused sweep graph really ran above
+    b = hz.solve(F, G, cfg)
+    assert (a.sweeps, a.total_transforms, a.big_transforms) == (b.sweeps, b.total_transforms, b.big_transforms)
+    for x, y in ((a.sigma, b.sigma), (a.U.re, b.U.re), (a.V.re, b.V.re), (a.Z.re, b.Z.re)):
+        assert np.array_equal(x, y)

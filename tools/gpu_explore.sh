@@ -1,5 +1,9 @@
 out=gpurun_out
 tag=${1:-x}
-timeout 900 python -m pytest tests -m gpu -x -q > $out/${tag}_pytest.log 2>&1; echo "rc $?" >> $out/${tag}_pytest.log
-python tools/phase_prof.py 4096 > $out/${tag}_phase.txt 2>&1
-timeout 600 python tools/explore.py 4096 cond 16 fb 100 >> $out/${tag}_explore.txt 2>&1
+HZG_SPLIT_ROWS=256 timeout 900 python -m pytest tests -m gpu -x -q -k "fused" > $out/${tag}_pytest_fused.log 2>&1; echo "rc $?" >> $out/${tag}_pytest_fused.log
+echo "fused split 256" >> $out/${tag}_explore.txt
+HZG_SPLIT_ROWS=256 timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
+echo "unfused split 256" >> $out/${tag}_explore.txt
+HZG_SPLIT_ROWS=256 HZG_FUSED=0 timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
+echo "unfused split 512" >> $out/${tag}_explore.txt
+HZG_FUSED=0 timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
