@@ -136,6 +136,27 @@ int hzg_launch_counts(const hzg_ctx* ctx, int64_t* per_sweep, int64_t* per_solve
  * counts4 = {divisions checked, mismatches, roots checked, mismatches}. */
 int hzg_test_fastmath(int64_t n, uint64_t seed, int64_t* counts4);
 
+/* Single block operations of the reference's public API, on device
+ * pointers (column-major planes), reference operation order (bitwise the
+ * reference), synchronous on `stream`:
+ *   hzg_op_grammian       -> _gram_of_pair / _k_grammian    (blocked.py:340-347, :40-56):
+ *                            the 2w x 2w Grammian of the m x 2w stack Y
+ *   hzg_op_cholesky_upper -> cholesky_upper                 (blocked.py:350-355, :59-94), in place
+ *   hzg_op_qr_shorten     -> qr_shorten                     (blocked.py:358-367, :97-217)
+ *   hzg_op_postmultiply   -> postmultiply                   (blocked.py:370-381, :220-250), Y in place
+ *   hzg_op_rescale        -> rescale_z                      (blocked.py:384-401, :253-295), in place;
+ *                            Z has mZ rows, sigF/sigG/sig written when final != 0 */
+int hzg_op_grammian(int64_t m, int32_t w, int32_t is_complex, int32_t compensated, const double* Yr,
+                    const double* Yi, double* Ar, double* Ai, void* stream);
+int hzg_op_cholesky_upper(int32_t tw, int32_t is_complex, double* Ar, double* Ai, void* stream);
+int hzg_op_qr_shorten(int64_t m, int32_t w, int32_t is_complex, const double* Yr, const double* Yi, double* Rr,
+                      double* Ri, void* stream);
+int hzg_op_postmultiply(int64_t m, int32_t w, int32_t is_complex, double* Yr, double* Yi, const double* Zr,
+                        const double* Zi, void* stream);
+int hzg_op_rescale(int64_t mF, int64_t mG, int64_t n, int32_t is_complex, int32_t compensated, int32_t final,
+                   double* Fr, double* Fi, double* Gr, double* Gi, double* Zr, double* Zi, int64_t mZ, double* sigF,
+                   double* sigG, double* sig, void* stream);
+
 const char* hzg_last_error(const hzg_ctx* ctx);
 void hzg_destroy(hzg_ctx* ctx);
 

@@ -11,6 +11,7 @@ from .core import (GsvdResult, MatrixPlanePair, ProblemPair, border_pair, read_m
                    write_matrix)
 from .errors import (DeviceError, FileFormatError, HzgsvdError, NotPositiveDefiniteError,
                      ProtocolError, RankError)
+from .ops import cholesky_upper, form_grammians, postmultiply, qr_shorten, rescale_z, run_distributed
 from .solver import DeviceGsvd, gsvd_1x1, gsvd_blocked, solve, upload_bordered
 from .strategies import (CommMapping, StrategyTable, block_moves, circle_positions, comm_mapping,
                          dump_table, gen_table, validate_table)
@@ -22,5 +23,6 @@ __all__ = [
     "read_matrix", "write_matrix", "DeviceError", "FileFormatError", "HzgsvdError",
     "NotPositiveDefiniteError", "ProtocolError", "RankError", "DeviceGsvd", "gsvd_1x1", "gsvd_blocked",
     "solve", "upload_bordered", "CommMapping", "StrategyTable", "block_moves", "circle_positions",
-    "comm_mapping", "dump_table", "gen_table", "validate_table",
+    "comm_mapping", "dump_table", "gen_table", "validate_table", "cholesky_upper", "form_grammians",
+    "postmultiply", "qr_shorten", "rescale_z", "run_distributed",
 ]

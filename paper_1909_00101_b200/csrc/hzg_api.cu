@@ -899,6 +899,122 @@ int hzg_launch_counts(const hzg_ctx* c, int64_t* per_sweep, int64_t* per_solve_f
   return HZG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Single block operations of the reference's public API (blocked.py:328-401),
+// reference-order (bitwise) device kernels.  Device pointers; synchronous.
+// ---------------------------------------------------------------------------
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 8); }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+}  // namespace
+
+int hzg_op_grammian(int64_t m, int32_t w, int32_t cplx, int32_t comp, const double* Yr, const double* Yi, double* Ar,
+                    double* Ai, void* stream) {
+  if (m < 1 || w < 1 || !Yr || !Ar || (cplx && (!Yi || !Ai))) return HZG_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int tw = 2 * w, NP = cplx ? 2 : 1;
+  Plane Y{const_cast<double*>(Yr), cplx ? const_cast<double*>(Yi) : nullptr, m, m};
+  GramWS gw{};
+  int nsplit = 1;
+  int64_t chunk = m;
+  if (!comp) gram_split(m, true, nsplit, chunk);
+  gw.nsplit[0] = gw.nsplit[1] = nsplit;
+  gw.chunk[0] = gw.chunk[1] = chunk;
+  gw.smax = nsplit;
+  const int64_t P = pow2c(m);
+  DevBuf cp, part, scr;
+  if (cp.alloc(8) || part.alloc((size_t)2 * nsplit * NP * tw * tw * 8) ||
+      (comp && scr.alloc((size_t)2 * 32 * P * 8)))
+    return HZG_CUDA;
+  const int32_t h_cp[2] = {0, w};
+  cudaMemcpyAsync(cp.p, h_cp, 8, cudaMemcpyHostToDevice, s);
+  StepPairs sp{(const int32_t*)cp.p, 1, 0, 1};
+  gw.part = (double*)part.p;
+  int rc = comp ? launch_gram_comp(Y, Y, sp, 0, w, cplx, gw, (double*)scr.p, P, s)
+                : launch_gram_exact(Y, Y, sp, 0, w, cplx, gw, s);
+  if (!rc) rc = launch_fold_gram(gw.part, nsplit, tw, cplx, Ar, cplx ? Ai : nullptr, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (rc) return rc;
+  return e == cudaSuccess ? HZG_OK : HZG_CUDA;
+}
+
+int hzg_op_cholesky_upper(int32_t tw, int32_t cplx, double* Ar, double* Ai, void* stream) {
+  if (tw < 1 || !Ar || (cplx && !Ai)) return HZG_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  DevBuf st;
+  if (st.alloc(4)) return HZG_CUDA;
+  int rc = launch_cholesky_op(tw, cplx, Ar, cplx ? Ai : nullptr, (int32_t*)st.p, s);
+  if (rc) return rc;
+  int32_t h = 0;
+  cudaMemcpyAsync(&h, st.p, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return HZG_CUDA;
+  return h ? HZG_NOT_PD : HZG_OK;
+}
+
+int hzg_op_qr_shorten(int64_t m, int32_t w, int32_t cplx, const double* Yr, const double* Yi, double* Rr,
+                      double* Ri, void* stream) {
+  if (m < 1 || w < 1 || !Yr || !Rr || (cplx && (!Yi || !Ri))) return HZG_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int tw = 2 * w;
+  Plane Y{const_cast<double*>(Yr), cplx ? const_cast<double*>(Yi) : nullptr, m, m};
+  DevBuf st, scr;
+  if (st.alloc(4) || scr.alloc((size_t)2 * m * tw * 8)) return HZG_CUDA;
+  double* Sr = (double*)scr.p;
+  int rc = launch_qr_op(Y, tw, cplx, Sr, Sr + m * tw, Rr, cplx ? Ri : nullptr, (int32_t*)st.p, s);
+  if (rc) return rc;
+  int32_t h = 0;
+  cudaMemcpyAsync(&h, st.p, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return HZG_CUDA;
+  return h ? HZG_RANK : HZG_OK;
+}
+
+int hzg_op_postmultiply(int64_t m, int32_t w, int32_t cplx, double* Yr, double* Yi, const double* Zr,
+                        const double* Zi, void* stream) {
+  if (m < 1 || w < 1 || !Yr || !Zr || (cplx && (!Yi || !Zi))) return HZG_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int tw = 2 * w, NP = cplx ? 2 : 1;
+  Plane Y{Yr, cplx ? Yi : nullptr, m, m};
+  Plane none{Yr, cplx ? Yi : nullptr, 0, m};  // rows = 0: the other two matrices are skipped
+  DevBuf cp, zt, id;
+  if (cp.alloc(8) || zt.alloc((size_t)NP * tw * tw * 8) || id.alloc(4)) return HZG_CUDA;
+  const int32_t h_cp[2] = {0, w};
+  cudaMemcpyAsync(cp.p, h_cp, 8, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(zt.p, Zr, (size_t)tw * tw * 8, cudaMemcpyDeviceToDevice, s);
+  if (cplx) cudaMemcpyAsync((double*)zt.p + tw * tw, Zi, (size_t)tw * tw * 8, cudaMemcpyDeviceToDevice, s);
+  cudaMemsetAsync(id.p, 0, 4, s);
+  StepPairs sp{(const int32_t*)cp.p, 1, 0, 1};
+  InnerOut io{(double*)zt.p, (int32_t*)id.p, nullptr, nullptr};
+  int rc = launch_postmult_exact(Y, none, none, sp, 0, w, cplx, io, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (rc) return rc;
+  return e == cudaSuccess ? HZG_OK : HZG_CUDA;
+}
+
+int hzg_op_rescale(int64_t mF, int64_t mG, int64_t n, int32_t cplx, int32_t comp, int32_t final, double* Fr,
+                   double* Fi, double* Gr, double* Gi, double* Zr, double* Zi, int64_t mZ, double* sigF,
+                   double* sigG, double* sig, void* stream) {
+  if (n < 1 || !Fr || !Gr || !Zr || (cplx && (!Fi || !Gi || !Zi)) || (final && (!sigF || !sigG || !sig)))
+    return HZG_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  Plane F{Fr, cplx ? Fi : nullptr, mF, mF}, G{Gr, cplx ? Gi : nullptr, mG, mG}, Z{Zr, cplx ? Zi : nullptr, mZ, mZ};
+  const int64_t P = pow2c(std::max(mF, mG));
+  DevBuf st, scr;
+  if (st.alloc(4) || (comp && scr.alloc((size_t)n * P * 8))) return HZG_CUDA;
+  cudaMemsetAsync(st.p, 0, 4, s);
+  int rc = launch_rescale(F, G, Z, n, cplx, final, sigF, sigG, sig, nullptr, (int32_t*)st.p,
+                          comp ? (double*)scr.p : nullptr, P, s);
+  if (rc) return rc;
+  int32_t h = 0;
+  cudaMemcpyAsync(&h, st.p, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return HZG_CUDA;
+  return h ? HZG_RANK : HZG_OK;
+}
+
 int hzg_test_fastmath(int64_t n, uint64_t seed, int64_t* counts4) {
   if (!counts4 || n < 1) return HZG_INVALID;
   return fastmath_check(n, seed, counts4);

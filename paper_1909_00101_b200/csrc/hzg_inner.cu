@@ -1005,7 +1005,56 @@ int launch_inner_t(const InnerParams& p, cudaStream_t s) {
   return launch_inner_g<TW, CPLX, false>(p, s);
 }
 
+// Single-block operations of the public API (cholesky_upper, qr_shorten,
+// blocked.py:345-363): the same device code the inner kernel uses.
+template <int TW, bool CPLX>
+__global__ void k_cholesky_op(double* Ar, double* Ai, int32_t* status) {
+  const int f = warp_cholesky<TW, CPLX, false>(Ar, Ai, threadIdx.x & 31);
+  if (threadIdx.x == 0) *status = f;
+}
+
+template <int TW, bool CPLX>
+__global__ void __launch_bounds__(256) k_qr_op(Plane Y, double* Sr, double* Si, double* outR, double* outI,
+                                              int32_t* status) {
+  __shared__ double qsh[3 * kMaxTW + 8];
+  const int bad = block_qr<TW, CPLX, false>(Y, 0, TW / 2, TW / 2, Sr, Si, outR, outI, qsh);
+  if (threadIdx.x == 0) *status = bad;
+}
+
 }  // namespace
+
+int launch_cholesky_op(int tw, int cplx, double* Ar, double* Ai, int32_t* status, cudaStream_t s) {
+#define HZG_CASE(T)                                                                      \
+  case T:                                                                                \
+    if (cplx) k_cholesky_op<T, true><<<1, 32, 0, s>>>(Ar, Ai, status);                   \
+    else k_cholesky_op<T, false><<<1, 32, 0, s>>>(Ar, Ai, status);                       \
+    break;
+  switch (tw) {
+    HZG_CASE(2) HZG_CASE(4) HZG_CASE(6) HZG_CASE(8) HZG_CASE(10) HZG_CASE(12) HZG_CASE(14) HZG_CASE(16)
+    HZG_CASE(20) HZG_CASE(24) HZG_CASE(32) HZG_CASE(48) HZG_CASE(64)
+    default:
+      return 4;
+  }
+#undef HZG_CASE
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+int launch_qr_op(const Plane& Y, int tw, int cplx, double* Sr, double* Si, double* outR, double* outI,
+                 int32_t* status, cudaStream_t s) {
+#define HZG_CASE(T)                                                                      \
+  case T:                                                                                \
+    if (cplx) k_qr_op<T, true><<<1, 256, 0, s>>>(Y, Sr, Si, outR, outI, status);         \
+    else k_qr_op<T, false><<<1, 256, 0, s>>>(Y, Sr, Si, outR, outI, status);             \
+    break;
+  switch (tw) {
+    HZG_CASE(2) HZG_CASE(4) HZG_CASE(6) HZG_CASE(8) HZG_CASE(10) HZG_CASE(12) HZG_CASE(14) HZG_CASE(16)
+    HZG_CASE(20) HZG_CASE(24) HZG_CASE(32) HZG_CASE(48) HZG_CASE(64)
+    default:
+      return 4;
+  }
+#undef HZG_CASE
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
 
 int launch_inner(const Plane& F, const Plane& G, const StepPairs& sp, int step, const KernelCfg& kc,
                  const GramWS& gw, const int32_t* itable, int isteps, const InnerOut& io, double* qr_scratch,

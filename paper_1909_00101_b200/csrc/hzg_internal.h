@@ -101,6 +101,11 @@ int launch_finalize(const Plane& U, const Plane& V, const Plane& Z, int64_t n, i
                     Plane Zo, double* sFo, double* sGo, double* so, int32_t* rank_ws, int32_t* status,
                     cudaStream_t s);
 
+int launch_fold_gram(const double* part, int nsplit, int tw, int cplx, double* Ar, double* Ai, cudaStream_t s);
+int launch_cholesky_op(int tw, int cplx, double* Ar, double* Ai, int32_t* status, cudaStream_t s);
+int launch_qr_op(const Plane& Y, int tw, int cplx, double* Sr, double* Si, double* outR, double* outI,
+                 int32_t* status, cudaStream_t s);
+
 bool dmma_supported(int w);
 int fastmath_check(int64_t n, uint64_t seed, int64_t* out4);
 

@@ -542,6 +542,39 @@ int launch_gram_comp(const Plane& F, const Plane& G, const StepPairs& sp, int st
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+// Fold the split partials of one block pair's Grammian (pairwise over the
+// splits, the reference's tree) and mirror it into a full tw x tw matrix
+// (blocked.py:40-56: lower = conj of upper, real diagonal).
+__global__ void k_fold_gram(const double* part, int nsplit, int tw, int cplx, double* Ar, double* Ai) {
+  const int NP = cplx ? 2 : 1;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tw * tw; e += gridDim.x * blockDim.x) {
+    const int r = e % tw, c = e / tw;
+    if (r > c) continue;
+    for (int pl = 0; pl < NP; ++pl) {
+      PairwiseAcc<24> acc;
+      acc.reset();
+      for (int q = 0; q < nsplit; ++q) acc.push(part[((int64_t)q * NP + pl) * tw * tw + e]);
+      const double v = acc.result();
+      if (pl == 0) {
+        Ar[c * tw + r] = v;
+        Ar[r * tw + c] = v;
+      } else {
+        Ai[c * tw + r] = r == c ? 0.0 : v;
+        Ai[r * tw + c] = r == c ? 0.0 : -v;
+      }
+    }
+    if (!cplx && Ai) {
+      Ai[c * tw + r] = 0.0;
+      Ai[r * tw + c] = 0.0;
+    }
+  }
+}
+
+int launch_fold_gram(const double* part, int nsplit, int tw, int cplx, double* Ar, double* Ai, cudaStream_t s) {
+  k_fold_gram<<<(tw * tw + 255) / 256, 256, 0, s>>>(part, nsplit, tw, cplx, Ar, Ai);
+  return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 int launch_counters(const int32_t* counts, int64_t nentries, int64_t* out, cudaStream_t s) {
   k_counters<<<1, 1024, 0, s>>>(counts, nentries, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;

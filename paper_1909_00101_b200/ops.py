@@ -1,0 +1,172 @@
+"""Single block operations of the reference's public API on the device.
+
+form_grammians, cholesky_upper, qr_shorten, postmultiply and rescale_z keep
+the reference's signatures and results (pkg/src/hzgsvd/blocked.py:328-401)
+and run the same reference-order kernels the solver uses (bitwise the
+reference), through the C ABI (include/hzg.h, hzg_op_*).  run_distributed
+(distsim.py:147) keeps its signature and runs the block-partitioned
+multi-rank schedule (dist.py) on the bordered pair.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .core import GsvdResult, MatrixPlanePair
+from .errors import DeviceError
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the B200 path has no CPU fallback")
+    return torch
+
+
+def _as_cols(Y):
+    Y = np.asarray(Y)
+    return Y.reshape(Y.shape[0], -1)
+
+
+def _dev_planes(a, cplx, torch):
+    """numpy (rows, cols) -> device column-major planes (cols, rows)."""
+    a = np.asarray(a)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    re = torch.from_numpy(np.ascontiguousarray(np.real(a).T, dtype=np.float64)).to(dev)
+    im = torch.from_numpy(np.ascontiguousarray(np.imag(a).T, dtype=np.float64)).to(dev) if cplx else None
+    return re, im
+
+
+def _host(re, im):
+    r = re.cpu().numpy().T
+    return r + 1j * im.cpu().numpy().T if im is not None else r.copy()
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _gram(stack, compensated, torch):
+    cplx = np.iscomplexobj(stack)
+    m, tw = stack.shape
+    Yr, Yi = _dev_planes(stack, cplx, torch)
+    Ar = torch.empty((tw, tw), dtype=torch.float64, device=Yr.device)
+    Ai = torch.empty((tw, tw), dtype=torch.float64, device=Yr.device) if cplx else None
+    L = _native.load()
+    _native.check(L.hzg_op_grammian(m, tw // 2, int(cplx), int(bool(compensated)), _p(Yr), _p(Yi), _p(Ar), _p(Ai),
+                                    _stream(torch)), None, "form_grammians")
+    return _host(Ar, Ai)
+
+
+def form_grammians(Fp, Fq, Gp, Gq, compensated=False):
+    """Grammians of the stacked block-column pairs [Fp Fq] and [Gp Gq]
+    (blocked.py:328-332)."""
+    torch = _torch()
+    A = _gram(np.hstack([_as_cols(Fp), _as_cols(Fq)]), compensated, torch)
+    B = _gram(np.hstack([_as_cols(Gp), _as_cols(Gq)]), compensated, torch)
+    return A, B
+
+
+def cholesky_upper(M):
+    """Upper Cholesky factor with positive real diagonal (blocked.py:350-355);
+    NotPositiveDefiniteError when the factorization breaks down."""
+    torch = _torch()
+    M = np.array(M)
+    cplx = np.iscomplexobj(M)
+    tw = M.shape[0]
+    Ar, Ai = _dev_planes(M, cplx, torch)
+    _native.check(_native.load().hzg_op_cholesky_upper(tw, int(cplx), _p(Ar), _p(Ai), _stream(torch)), None,
+                  "matrix is not numerically positive definite")
+    return _host(Ar, Ai)
+
+
+def qr_shorten(Yp, Yq):
+    """R factor (nonnegative diagonal) of the stacked block-column pair
+    (blocked.py:358-367); RankError on rank deficiency."""
+    torch = _torch()
+    stack = np.hstack([_as_cols(Yp), _as_cols(Yq)])
+    cplx = np.iscomplexobj(stack)
+    m, tw = stack.shape
+    Yr, Yi = _dev_planes(stack, cplx, torch)
+    Rr = torch.empty((tw, tw), dtype=torch.float64, device=Yr.device)
+    Ri = torch.empty((tw, tw), dtype=torch.float64, device=Yr.device) if cplx else None
+    _native.check(_native.load().hzg_op_qr_shorten(m, tw // 2, int(cplx), _p(Yr), _p(Yi), _p(Rr), _p(Ri),
+                                                   _stream(torch)), None,
+                  "rank-deficient block columns in the QR shortening")
+    return _host(Rr, Ri)
+
+
+def postmultiply(Yp, Yq, Ztilde):
+    """[Yp' Yq'] = [Yp Yq] Ztilde (blocked.py:370-381)."""
+    torch = _torch()
+    Yp = _as_cols(Yp)
+    w = Yp.shape[1]
+    stack = np.hstack([Yp, _as_cols(Yq)])
+    Zt = np.asarray(Ztilde)
+    cplx = np.iscomplexobj(stack) or np.iscomplexobj(Zt)
+    if cplx:
+        stack = stack.astype(np.complex128)
+        Zt = Zt.astype(np.complex128)
+    m = stack.shape[0]
+    Yr, Yi = _dev_planes(stack, cplx, torch)
+    Zr, Zi = _dev_planes(Zt, cplx, torch)
+    _native.check(_native.load().hzg_op_postmultiply(m, w, int(cplx), _p(Yr), _p(Yi), _p(Zr), _p(Zi),
+                                                     _stream(torch)), None, "postmultiply")
+    out = _host(Yr, Yi)
+    return out[:, :w], out[:, w:]
+
+
+def rescale_z(F, G, Z, final=False, compensated=False):
+    """Theta rescaling of Z; with ``final`` also returns (U, V, Z, sigF, sigG,
+    sigma) (blocked.py:384-401).  F, G, Z are MatrixPlanePair values."""
+    torch = _torch()
+    cplx = F.is_complex
+    dF = _dev_planes(F.to_dense(), cplx, torch)
+    dG = _dev_planes(G.to_dense(), cplx, torch)
+    dZ = _dev_planes(Z.to_dense().astype(np.complex128) if cplx else Z.to_dense(), cplx, torch)
+    n = F.cols
+    kw = dict(dtype=torch.float64, device=dF[0].device)
+    sig = [torch.empty(n, **kw) for _ in range(3)]
+    L = _native.load()
+    _native.check(L.hzg_op_rescale(F.rows, G.rows, n, int(cplx), int(bool(compensated)), int(bool(final)),
+                                   _p(dF[0]), _p(dF[1]), _p(dG[0]), _p(dG[1]), _p(dZ[0]), _p(dZ[1]), Z.rows,
+                                   _p(sig[0]), _p(sig[1]), _p(sig[2]), _stream(torch)), None,
+                  "zero column during rescaling")
+    Zo = MatrixPlanePair.from_dense(_host(*dZ))
+    if not final:
+        return Zo
+    return (MatrixPlanePair.from_dense(_host(*dF)), MatrixPlanePair.from_dense(_host(*dG)), Zo,
+            sig[0].cpu().numpy(), sig[1].cpu().numpy(), sig[2].cpu().numpy())
+
+
+def run_distributed(p, cfg=None, s=2, s_inner=1, pool=1):
+    """Solve a bordered pair with s ranks (distsim.py:147 signature).
+
+    The B200 build distributes column blocks over ranks with the
+    block-partitioned schedule (dist.py); the result is bitwise that of a
+    single rank, i.e. of gsvd_blocked (columns in their original order).
+    ``s_inner`` and ``pool`` are accepted for signature compatibility."""
+    from .config import SolverConfig
+    from .dist import PartitionedGsvd
+    from .solver import _result_from_device, upload_bordered
+
+    cfg = cfg or SolverConfig()
+    if s < 1:
+        raise ValueError("need at least one worker")
+    w = cfg.block_width
+    if p.n % (2 * w * s) != 0:
+        raise ValueError("n=%d not divisible for %d workers at block width %d" % (p.n, s, w))
+    planes, n, mF, mG = upload_bordered(p.F, p.G, w)
+    job = PartitionedGsvd(planes, cfg, s)
+    try:
+        job.run()
+        out = job.finalize(n, p.F.rows, p.G.rows, sort=False)
+        r = _result_from_device(job.devs[0], out, p.is_complex, workers=s)
+        return r
+    finally:
+        job.close()
