@@ -327,3 +327,21 @@ def test_fused_postgram_bitwise_equals_unfused(name, monkeypatch):
     assert (a.sweeps, a.total_transforms, a.big_transforms) == (b.sweeps, b.total_transforms, b.big_transforms)
     for x, y in ((a.sigma, b.sigma), (a.U.re, b.U.re), (a.V.re, b.V.re), (a.Z.re, b.Z.re)):
         assert np.array_equal(x, y)
+
+
+def test_wavefront_groups_bitwise_invariant(monkeypatch):
+    """The sweep graph's circle-position groups (streams overlapping the
+    steps of neighbouring groups) must not change a single bit: same
+    solve with 1, 2, 4 and 8 groups (n = 1024, 32 pairs per step)."""
+    g = O.gaussian_stream(91, 2 * 1024 * 1024)
+    F = g[: 1024 * 1024].reshape((1024, 1024), order="F")
+    G = g[1024 * 1024:].reshape((1024, 1024), order="F")
+    cfg = hz.SolverConfig(block_width=16)
+    runs = []
+    for groups in ("1", "2", "4", "8"):
+        monkeypatch.setenv("HZG_GROUPS", groups)
+        runs.append(hz.solve(F, G, cfg))
+    for r in runs[1:]:
+        assert (r.sweeps, r.total_transforms, r.big_transforms) == \
+            (runs[0].sweeps, runs[0].total_transforms, runs[0].big_transforms)
+        assert np.array_equal(r.sigma, runs[0].sigma) and np.array_equal(r.Z.re, runs[0].Z.re)
