@@ -177,10 +177,11 @@ int cuda_fail(hzg_ctx* c, cudaError_t e, const char* where) {
 
 // Grammian split geometry per matrix height (depends on m only, never on
 // the GPU count, so results are GPU-count invariant).
-// rows per Grammian split in DMMA mode (HZG_SPLIT_ROWS, for tuning)
+// rows per Grammian split in DMMA mode: HZG_SPLIT_ROWS fixes them (the
+// fused postmultiply + Grammian needs <= 256); 0 = default geometry
 int64_t split_rows() {
   const char* e = std::getenv("HZG_SPLIT_ROWS");
-  return e ? std::max<int64_t>(64, std::atoi(e)) / 64 * 64 : 512;
+  return e ? std::max<int64_t>(64, std::atoi(e)) / 64 * 64 : 0;
 }
 
 void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
@@ -190,10 +191,12 @@ void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
     chunk = std::max<int64_t>(32, std::min<int64_t>(P, 2048));
     nsplit = (int)std::max<int64_t>(1, P / chunk);
   } else {
-    // splits of at most 512 rows (a power-of-two count; the fused
-    // postmultiply + Grammian keeps a split's half tiles on chip), chunk a
-    // multiple of 64 rows.  Depends on m only, never on the GPU count.
-    nsplit = (int)pow2c((m + kSplitRows - 1) / kSplitRows);
+    // >= 512 rows per split CTA and at most 8 splits (partials stay a few
+    // percent of the Grammian's reads), or the fixed HZG_SPLIT_ROWS; a
+    // power-of-two count, chunk a multiple of 64 rows.  Depends on m only,
+    // never on the GPU count.
+    nsplit = kSplitRows > 0 ? (int)pow2c((m + kSplitRows - 1) / kSplitRows)
+                            : (int)std::min<int64_t>(8, pow2c((m + 511) / 512));
     chunk = ((m + nsplit - 1) / nsplit + 63) / 64 * 64;
   }
 }

@@ -11,16 +11,21 @@ def launches(path):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr = rows[hi]
-    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-    agg = collections.defaultdict(list)
+    ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+    agg = collections.defaultdict(lambda: collections.defaultdict(list))
     for r in rows[hi + 1:]:
         name = r[ki].split("(")[0].replace("void ", "").replace("hzg::<unnamed>::", "")
-        agg[name].append(float(r[vi].replace(",", "")))
-    tot = sum(sum(v) for v in agg.values())
-    out = ["launch list: %s (gpu__time_duration.sum, --clock-control none; serialised, cold-cache)" % path,
-           "%-36s %6s %12s %8s" % ("kernel", "n", "avg us", "share")]
-    for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-        out.append("%-36s %6d %12.2f %8.3f" % (k[:36], len(v), sum(v) / len(v) / 1e3, sum(v) / tot))
+        agg[name][r[mi]].append(float(r[vi].replace(",", "")))
+    T = "gpu__time_duration.sum"
+    tot = sum(sum(d[T]) for d in agg.values())
+    out = ["launch list: %s (--clock-control none; serialised, cold-cache)" % path,
+           "%-36s %6s %12s %8s %12s %10s" % ("kernel", "n", "avg us", "share", "DRAM MB/l", "TB/s")]
+    for k, d in sorted(agg.items(), key=lambda x: -sum(x[1][T])):
+        t = d[T]
+        b = [x + y for x, y in zip(d.get("dram__bytes_read.sum", []), d.get("dram__bytes_write.sum", []))]
+        mb = sum(b) / len(b) / 1e6 if b else float("nan")
+        out.append("%-36s %6d %12.2f %8.3f %12.1f %10.2f" % (k[:36], len(t), sum(t) / len(t) / 1e3, sum(t) / tot, mb,
+                                                         (sum(b) / sum(t) / 1e3) if b else float("nan")))
     return out
 
 
