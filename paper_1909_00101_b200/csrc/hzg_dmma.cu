@@ -13,6 +13,9 @@
 //
 // Tolerance parity only: DMMA accumulates in a different order from the
 // reference's pairwise trees (blocked.py:40-56) and fma chains (:220-250).
+#include <algorithm>
+#include <cstdlib>
+
 #include "hzg_device.cuh"
 #include "hzg_internal.h"
 
@@ -920,7 +923,10 @@ int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const S
   int64_t mmax = 0;
   const Plane* Y[3] = {&F, &G, &Z};
   for (int q = mat0; q < mat0 + nmats; ++q) mmax = Y[q]->rows > mmax ? Y[q]->rows : mmax;
-  PostParams p{{F, G, Z}, sp, step, io, 1024, mat0};
+  // rows per CTA (HZG_POST_CHUNK, multiple of 64, for tuning)
+  int64_t chunk = 1024;
+  if (const char* e = std::getenv("HZG_POST_CHUNK")) chunk = std::max(64, std::atoi(e)) / 64 * 64;
+  PostParams p{{F, G, Z}, sp, step, io, chunk, mat0};
   switch (2 * w) {
     case 16:
       return cplx ? post_ws_t<16, true>(p, mmax, nmats, s) : post_ws_t<16, false>(p, mmax, nmats, s);
