@@ -105,17 +105,27 @@ class DistTransport:
 
     def exchange(self, moves):
         dist = self.dist
-        ops = []
+        # NCCL moves device tensors directly; a gloo group (CPU tests, or
+        # several ranks sharing one GPU) stages device blocks through host
+        # memory
+        staged = dist.get_backend(self.group) == "gloo"
+        ops, back = [], []
         for (b, src, dst) in moves:
             if src == self.rank:
                 for t in _block_views(self.planes, b, self.w):
-                    ops.append(dist.P2POp(dist.isend, t, dst, self.group))
+                    ops.append(dist.P2POp(dist.isend, t.cpu() if staged and t.is_cuda else t, dst, self.group))
             elif dst == self.rank:
                 for t in _block_views(self.planes, b, self.w):
+                    if staged and t.is_cuda:
+                        h = t.new_empty(t.shape, device="cpu")
+                        back.append((t, h))
+                        t = h
                     ops.append(dist.P2POp(dist.irecv, t, src, self.group))
         if ops:
             for wk in dist.batch_isend_irecv(ops):
                 wk.wait()
+        for t, h in back:
+            t.copy_(h)
 
 
 def gather_blocks(sched, k_final=0):
@@ -196,8 +206,10 @@ class PartitionedGsvd:
             self.devs = [dev]
             self.transport = DistTransport(dict(planes, Zr=dev.Zr, Zi=dev.Zi), w, self.rank)
 
+            cdev = "cpu" if dist.get_backend() == "gloo" else dev.device
+
             def allreduce(t, b):
-                x = torch.tensor([t, b], dtype=torch.int64, device=dev.device)
+                x = torch.tensor([t, b], dtype=torch.int64, device=cdev)
                 dist.all_reduce(x)
                 return int(x[0]), int(x[1])
 
