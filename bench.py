@@ -1,28 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the B200 GSVD path (BASELINE.json metric: GSVD wall time and
-FP64 GFLOP/s).
+FP64 GFLOP/s at n = 4096 / 16384 on 1/2/4/8 B200 vs CPU).
 
-A step is one complete GSVD of the configured synthetic pair: prescale, all
-outer sweeps to convergence, final rescale, unborder and sort.
+Workload (default): config 5 -- a real FP64 iid-Gaussian pair F, G of order
+16384, block width 16.  A step is ONE OUTER SWEEP of the blocked GSVD (all
+n/w - 1 outer steps: Grammians, inner solves, postmultiplies, the counter
+fold and the inter-sweep rescale); W warm-up sweeps follow the prescale,
+then K sweeps are timed.  On N > 1 GPUs (torchrun) the same problem's
+column blocks are partitioned over the ranks (strong scaling) with an NCCL
+block exchange after every outer step.
 
-* value  -- inputs resident in HBM (device-to-device refresh of the working
-            planes is inside the step), outputs left in HBM; FP64 GFLOP/s of
-            the algorithmic count:
-            sweeps * P * c * [12 w^2 (mF + mG) + 8 w^2 n],  P = Nb (Nb - 1) / 2.
-* e2e    -- the same through the public drop-in API solve(): numpy inputs in
-            pinned host memory copied in, numpy U, V, Z, sigma copied out.
-* roofline -- the step kernels run alone over sweep 1 of the same pair
-            (one launch per outer step covering every block pair, CUDA
-            events on the launch stream): algorithmic bytes per launch /
-            average duration, against the measured HBM copy bandwidth.
-* n16384  -- config 5 (iid Gaussian 16384^2) timed over its first sweeps.
+* value  -- FP64 GFLOP/s of the algorithmic count per sweep:
+            F_sweep = P * c * [12 w^2 (mF + mG) + 8 w^2 n],  P = Nb (Nb - 1) / 2;
+            inputs resident in HBM (F + G + Z = 6.4 GB >> L2).
+* e2e    -- the public drop-in API solve() on numpy inputs in pinned host
+            memory, capped at --e2e-sweeps sweeps (copies in, sweeps,
+            final rescale / unborder / sort, copies out), same GFLOP/s count.
+* roofline -- the step kernels alone over sweep 1 (one launch per outer
+            step covering every pair, CUDA events on the launch stream):
+            algorithmic bytes per launch / average duration vs the measured
+            HBM copy bandwidth; plus the FP64 fraction of the whole step.
+* config4 -- a full GSVD (to convergence) of config 4 (real 4096^2,
+            sigma in [1e-8, 1e8]): wall time, sweeps, accuracy.
 * cpu_baseline -- the CPU oracle (C restatement, bitwise the reference) on
             a bounded sample of outer steps, all host threads.
 
 `--impl reference` times the reference CPU path (the oracle port) alone.
-Multi-GPU (torchrun, N > 1): ONE problem whose column blocks are partitioned
-over the N ranks (strong scaling), blocks exchanged with NCCL send/recv
-every outer step; the time is the max over ranks.
 """
 
 import argparse
@@ -47,20 +50,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--size", dest="n", type=int, default=4096, help="matrix order n (config 4: 4096)")
-    ap.add_argument("--kind", default="cond", choices=["cond", "gauss"],
-                    help="cond: config 4 (sigma in [1e-8, 1e8]); gauss: iid Gaussian (config 5)")
+    ap.add_argument("--size", dest="n", type=int, default=16384, help="matrix order n (config 5: 16384)")
+    ap.add_argument("--kind", default="gauss", choices=["cond", "gauss"],
+                    help="gauss: iid Gaussian (config 5); cond: config 4 (sigma in [1e-8, 1e8])")
     ap.add_argument("--w", type=int, default=16)
     ap.add_argument("--seed", type=int, default=4096)
-    ap.add_argument("--max-sweeps", type=int, default=None,
-                    help="outer sweep cap (default: 30, the reference's; 100 for the ill-conditioned config so "
-                         "the solve runs to convergence)")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--e2e-sweeps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--big-n", type=int, default=16384,
-                    help="also time the first --big-sweeps sweeps of config 5 at this n (0: skip)")
-    ap.add_argument("--big-sweeps", type=int, default=2)
+    ap.add_argument("--config4-size", type=int, default=4096, help="full-solve extra of config 4 (0: skip)")
     return ap.parse_args()
 
 
@@ -71,9 +70,9 @@ def parse():
 def workload_name(a):
     if a.kind == "cond":
         return ("config4: real FP64 F,G %dx%d, generalized singular values logspace(1e-8,1e8) shuffled, "
-                "F=U diag(sF) X, G=V diag(sG) X (U,V Haar, X=W diag(U[0.01,1]) W^T), w=%d, full GSVD per step"
-                % (a.n, a.n, a.w))
-    return "real FP64 iid-Gaussian F,G %dx%d, w=%d, full GSVD per step" % (a.n, a.n, a.w)
+                "F=U diag(sF) X, G=V diag(sG) X (U,V Haar, X=W diag(U[0.01,1]) W^T), w=%d, one outer sweep "
+                "per step" % (a.n, a.n, a.w))
+    return "config5: real FP64 iid-Gaussian F,G %dx%d, w=%d, one outer sweep per step" % (a.n, a.n, a.w)
 
 
 def gen_pair(a, torch, device):
@@ -160,23 +159,23 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def cpu_sample(Fp, Gp, w, cfg_kw, budget_s, threads):
-    """Time outer steps of sweep 1 of the oracle on the bordered planes.
-    Returns (steps, seconds, flops)."""
-    import numpy as np
+    """Time outer steps of sweep 1 of the oracle on the bordered planes (the
+    oracle's own clock around the steps; its per-call set-up -- plane copies,
+    prescale -- is excluded).  Returns (steps, seconds, flops)."""
     from oracle import oracle as O
     n, mF = Fp.shape[1], Fp.shape[0]
     mG = Gp.shape[0]
     cfg = O.make_cfg(block_width=w, **cfg_kw)
     osteps = n // w - 1
     per_step = flops_per_sweep(n, mF, mG, w) / osteps
-    t0 = time.perf_counter()
-    O.gsvd_blocked(Fp, None, Gp, None, False, cfg, threads=threads, step_limit=1)
-    t1 = time.perf_counter() - t0
+    r = O.gsvd_blocked(Fp, None, Gp, None, False, cfg, threads=threads, step_limit=1)
+    t1 = r["step_seconds"]
     steps = int(max(1, min(osteps, budget_s / max(t1, 1e-3))))
-    t0 = time.perf_counter()
-    O.gsvd_blocked(Fp, None, Gp, None, False, cfg, threads=threads, step_limit=steps)
-    dt = time.perf_counter() - t0
-    return steps, dt, steps * per_step
+    if steps > 1:
+        r = O.gsvd_blocked(Fp, None, Gp, None, False, cfg, threads=threads, step_limit=steps)
+    else:
+        steps = 1
+    return steps, r["step_seconds"], steps * per_step
 
 
 def run_reference(a):
@@ -189,16 +188,21 @@ def run_reference(a):
     Fr, Gr, _ = gen_pair(a, torch, "cpu")
     Fp = np.asfortranarray(Fr.numpy().T)
     Gp = np.asfortranarray(Gr.numpy().T)
+    from oracle import oracle as O
     threads = os.cpu_count() or 1
-    per = max(1.0, a.cpu_seconds / max(1, a.steps + a.warmup))
-    for _ in range(a.warmup):
-        cpu_sample(Fp, Gp, a.w, {}, per, threads)
+    per = max(1.0, a.cpu_seconds / max(1, a.steps))
+    # warm-up calls also size the sample: outer steps per bench step
+    k = 1
+    for _ in range(max(1, a.warmup)):
+        k, _, _ = cpu_sample(Fp, Gp, a.w, {}, per, threads)
+    cfg = O.make_cfg(block_width=a.w)
+    per_step = flops_per_sweep(a.n, a.n, a.n, a.w) / (a.n // a.w - 1)
     tot_t, tot_f, tot_s = 0.0, 0.0, 0
     for _ in range(a.steps):
-        s, dt, fl = cpu_sample(Fp, Gp, a.w, {}, per, threads)
-        tot_t += dt
-        tot_f += fl
-        tot_s += s
+        r = O.gsvd_blocked(Fp, None, Gp, None, False, cfg, threads=threads, step_limit=k)
+        tot_t += r["step_seconds"]
+        tot_f += k * per_step
+        tot_s += k
     v = tot_f / tot_t / 1e9
     n = a.n
     osteps = n // a.w - 1
@@ -209,7 +213,8 @@ def run_reference(a):
             "config": {"workload": workload_name(a), "n": n, "block_width": a.w,
                        "sample": "%d outer steps of sweep 1 in total (of %d per sweep)" % (tot_s, osteps)},
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-                             "sample": "%d outer steps of sweep 1, %d threads" % (tot_s, threads)},
+                             "sample": "%d outer steps of sweep 1 (%d per bench step), %d threads; the oracle's "
+                                       "clock around its outer steps" % (tot_s, k, threads)},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "est_full_sweep_s": tot_t / tot_s * osteps}
     print(json.dumps(line), flush=True)
@@ -250,39 +255,47 @@ def sweep_bytes(n, mF, mG, w):
     return P * (48 * w * (mF + mG) + 32 * w * n)
 
 
-def big_sweeps(hz, torch, device, n, w, sweeps, seed):
-    """Config 5 (iid Gaussian n x n) bounded to its first `sweeps` outer
-    sweeps (the heaviest ones): FP64 GFLOP/s of the algorithmic count."""
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    F = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
-    G = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
-    cfg = hz.SolverConfig(block_width=w)
-    dev = hz.DeviceGsvd({"Fr": F, "Gr": G, "Fi": None, "Gi": None}, cfg)
-    dev.init()
-    dev.sweep()  # builds the graph; sweep 1 (also timed below from a fresh start)
-    F2 = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
-    G2 = torch.randn((n, n), generator=g, dtype=torch.float64, device=device)
-    F.copy_(F2)
-    G.copy_(G2)
-    del F2, G2
+def config4_full(hz, torch, device, n, w, seed):
+    """Full GSVD of config 4 (to convergence): wall time, sweeps, accuracy."""
+    class A:
+        pass
+    c = A()
+    c.n, c.kind, c.seed, c.w = n, "cond", seed, w
+    F0, G0, truth = gen_pair(c, torch, device)
+    cfg = hz.SolverConfig(block_width=w, max_outer_sweeps=100)
+    Fw, Gw = torch.empty_like(F0), torch.empty_like(G0)
+    dev = hz.DeviceGsvd({"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}, cfg)
+
+    def once():
+        Fw.copy_(F0)
+        Gw.copy_(G0)
+        dev.run()
+        return dev.finalize(n, n, n)
+
+    once()  # warm-up (graph build)
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    dev.init()
-    for _ in range(sweeps):
-        dev.sweep()
+    out = once()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    fl = sweeps * flops_per_sweep(n, n, n, w)
+    s = e0.elapsed_time(e1) / 1e3
+    fl = dev.sweeps * flops_per_sweep(n, n, n, w)
+    Ur, Vr, Zr = out["Ur"], out["Vr"], out["Zr"]
+    sF, sG = out["sigmaF"], out["sigmaG"]
+    Fm, Gm = F0.T, G0.T
+    eye = torch.eye(n, dtype=torch.float64, device=device)
+    tr = torch.sort(truth, descending=True).values
+    acc = {"resF": float(torch.linalg.norm(Fm @ Zr.T - Ur.T * sF[None, :]) / torch.linalg.norm(Fm)),
+           "resG": float(torch.linalg.norm(Gm @ Zr.T - Vr.T * sG[None, :]) / torch.linalg.norm(Gm)),
+           "orthU": float(torch.linalg.norm(Ur @ Ur.T - eye)), "orthV": float(torch.linalg.norm(Vr @ Vr.T - eye)),
+           "normalization": float(torch.max(torch.abs(sF * sF + sG * sG - 1))),
+           "max_rel_sigma_vs_generator": float(torch.max(torch.abs(out["sigma"] - tr) / tr))}
     dev.close()
-    return {"workload": "config5: real FP64 iid-Gaussian F,G %dx%d, w=%d, first %d outer sweeps from the "
-                        "prescale (the heaviest sweeps; a full solve needs ~30+)" % (n, n, w, sweeps),
-            "s_per_sweep": ms / 1e3 / sweeps, "gflops": fl / (ms / 1e3) / 1e9,
-            "fp64_frac": fl / (ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
-            "hbm_gbs_algorithmic": sweeps * sweep_bytes(n, n, n, w) / (ms / 1e3) / 1e9}
+    return {"workload": "config4: real FP64 F,G %dx%d, sigma logspace(1e-8,1e8), w=%d, full GSVD to convergence "
+                        "(inputs in HBM)" % (n, n, w),
+            "wall_s": s, "sweeps": dev.sweeps, "converged": bool(dev.converged), "gflops": fl / s / 1e9,
+            "fp64_frac": fl / s / 1e12 / FP64_PEAK_TFLOPS, "accuracy": acc}
 
 
 def main():
@@ -312,36 +325,33 @@ def main():
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group(backend)
-
-    # every rank generates the same pair; N > 1 partitions its column blocks
-    Fr0, Gr0, truth = gen_pair(a, torch, device)
-    n = a.n
-    cap = a.max_sweeps if a.max_sweeps else (100 if a.kind == "cond" else 30)
-    cfg = hz.SolverConfig(block_width=a.w, max_outer_sweeps=cap)
-    w = a.w
-    assert n % (2 * w) == 0, "bench uses n divisible by 2w"
-    mF = mG = n
-    Fw = torch.empty_like(Fr0)
-    Gw = torch.empty_like(Gr0)
-    planes = {"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}
-    if world > 1:
-        job = PartitionedGsvd(planes, cfg, world, comm="dist")
-    else:
-        job = hz.DeviceGsvd(planes, cfg)
-    F_sweep = flops_per_sweep(n, mF, mG, w)
-
-    def step():
-        Fw.copy_(Fr0)
-        Gw.copy_(Gr0)
-        job.run()
-        return job.finalize(n, mF, mG)
+    cdev = device if backend == "nccl" else "cpu"
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    for _ in range(max(3, a.warmup)):
-        out = step()
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device=cdev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # every rank generates the same pair; N > 1 partitions its column blocks
+    Fr0, Gr0, truth = gen_pair(a, torch, device)
+    n, w = a.n, a.w
+    assert n % (2 * w) == 0, "bench uses n divisible by 2w"
+    mF = mG = n
+    cfg = hz.SolverConfig(block_width=w, max_outer_sweeps=100)
+    Fw, Gw = Fr0.clone(), Gr0.clone()
+    planes = {"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}
+    job = PartitionedGsvd(planes, cfg, world, comm="dist") if world > 1 else hz.DeviceGsvd(planes, cfg)
+    F_sweep = flops_per_sweep(n, mF, mG, w)
+
+    job.init()
+    W = max(3, a.warmup)
+    for _ in range(W):
+        job.sweep()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     barrier()
@@ -350,42 +360,18 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    sweeps = []
     for _ in range(a.steps):
-        out = step()
-        sweeps.append(job.sweeps)
+        job.sweep()
     e1.record()
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    cdev = device if backend == "nccl" else "cpu"
-    t = torch.tensor([ms], dtype=torch.float64, device=cdev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    # one problem for the whole job: the flops are counted once
-    flops = sum(s * F_sweep for s in sweeps)
-    value = flops / (ms_max / 1e3) / 1e9
+    ms_max = max_over_ranks(e0.elapsed_time(e1))
+    value = a.steps * F_sweep / (ms_max / 1e3) / 1e9  # one problem for the whole job
     per_sweep_launches, fixed_launches = job.launch_counts()
-    launches = sum(s * per_sweep_launches + fixed_launches for s in sweeps)
-
-    # accuracy of the last solve (self-consistency + truth), on the GPU
-    acc = {}
-    if rank == 0:
-        Ur, Vr, Zr = out["Ur"], out["Vr"], out["Zr"]
-        sF, sG, s = out["sigmaF"], out["sigmaG"], out["sigma"]
-        Fm, Gm = Fr0.T, Gr0.T
-        Zm = Zr.T
-        acc["resF"] = float(torch.linalg.norm(Fm @ Zm - Ur.T * sF[None, :]) / torch.linalg.norm(Fm))
-        acc["resG"] = float(torch.linalg.norm(Gm @ Zm - Vr.T * sG[None, :]) / torch.linalg.norm(Gm))
-        eye = torch.eye(n, dtype=torch.float64, device=device)
-        acc["orthU"] = float(torch.linalg.norm(Ur @ Ur.T - eye))
-        acc["orthV"] = float(torch.linalg.norm(Vr @ Vr.T - eye))
-        acc["normalization"] = float(torch.max(torch.abs(sF * sF + sG * sG - 1)))
-        if truth is not None:
-            tr = torch.sort(truth, descending=True).values
-            acc["max_rel_sigma_vs_generator"] = float(torch.max(torch.abs(s - tr) / tr))
+    launches = a.steps * per_sweep_launches
+    job.close()
+    del job
 
     # e2e through the public drop-in API with pinned host buffers
     ke = a.e2e_steps if a.e2e_steps is not None else max(1, min(a.steps, 3))
@@ -395,31 +381,28 @@ def main():
     Gh.copy_(Gr0)
     Fnp = Fh.numpy().T  # Fortran-order (m, n) views of pinned memory
     Gnp = Gh.numpy().T
+    ecfg = hz.SolverConfig(block_width=w, max_outer_sweeps=a.e2e_sweeps)
     if world > 1:
         from paper_1909_00101_b200.dist import solve_blocks
 
         def api():
-            return solve_blocks(Fnp, Gnp, cfg, world, comm="dist")
+            return solve_blocks(Fnp, Gnp, ecfg, world, comm="dist")
     else:
         def api():
-            return hz.solve(Fnp, Gnp, cfg)
-    r = api()  # warm
+            return hz.solve(Fnp, Gnp, ecfg)
+    api()  # warm
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    e2e_sweeps = []
+    e2e_sweeps = 0
     for _ in range(ke):
         r = api()
         if r is not None:
-            e2e_sweeps.append(r.sweeps)
+            e2e_sweeps += r.sweeps
     torch.cuda.synchronize()
     barrier()
-    te = time.perf_counter() - t0
-    tt = torch.tensor([te], dtype=torch.float64, device=cdev)
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    te = float(tt.item())
-    e2e_value = sum(s * F_sweep for s in e2e_sweeps) / te / 1e9 if e2e_sweeps else None
+    te = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = e2e_sweeps * F_sweep / te / 1e9 if e2e_sweeps else None
     h2d = (mF + mG) * n * 8
     d2h = (mF + mG + n) * n * 8 + 3 * n * 8
 
@@ -433,7 +416,7 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     Fw.copy_(Fr0)
     Gw.copy_(Gr0)
-    kt, bpl = isolated_kernels(hz, planes, cfg, n, mF, mG, w, n // w - 1)
+    kt, bpl = isolated_kernels(hz, planes, hz.SolverConfig(block_width=w), n, mF, mG, w, n // w - 1)
     avg = {k: v[0] / max(1, v[1]) for k, v in kt.items()}
     tot_k = sum(v[0] for v in kt.values())
     post_gbs = bpl["postmult"] / (avg["postmult"] / 1e3) / 1e9
@@ -443,26 +426,25 @@ def main():
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
             traffic = json.load(fh).get("postmult_dram_bytes_per_launch")
-    step_bytes = sum(s * sweep_bytes(n, mF, mG, w) for s in sweeps)
     roofline = {"kernel": "k_post_ws (postmultiply of F, G, Z block pairs; the dominant HBM-bound kernel)",
                 "bound": "hbm", "achieved": post_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": post_gbs / hbm_peak, "traffic": traffic, "peak_source": peak_src,
                 "bytes_per_launch": bpl["postmult"], "avg_launch_ms": avg["postmult"],
-                "measured": "isolated: sweep 1 of this pair, one launch per step covering all %d pairs, "
+                "measured": "isolated: sweep 1 of this pair, one launch per outer step covering all %d pairs, "
                             "CUDA events on the launch stream" % (n // w // 2),
                 "grammian": {"achieved": gram_gbs, "frac": gram_gbs / hbm_peak, "bytes_per_launch": bpl["grammian"],
                              "avg_launch_ms": avg["grammian"]},
                 "inner": {"avg_launch_ms": avg["inner"], "bound": "latency (dependent FP64 div/sqrt chains + "
                                                                  "one CTA barrier per inner step)"},
                 "kernel_time_shares_isolated": {k: v[0] / tot_k for k, v in kt.items()} if tot_k else {},
-                "timed_region_hbm_gbs": step_bytes / (ms_max / 1e3) / 1e9,
+                "timed_region_hbm_gbs": a.steps * sweep_bytes(n, mF, mG, w) / (ms_max / 1e3) / 1e9,
                 "fp64": {"achieved_tflops": value / 1e3, "peak_tflops": FP64_PEAK_TFLOPS,
                          "peak_source": "profiles/r01_fp64_peak.txt (DMMA microbenchmark on this pool's B200)",
                          "frac": value / 1e3 / FP64_PEAK_TFLOPS}}
 
     extra = None
-    if world == 1 and a.big_n > 0:
-        extra = big_sweeps(hz, torch, device, a.big_n, w, a.big_sweeps, a.seed + 1)
+    if world == 1 and a.config4_size > 0:
+        extra = config4_full(hz, torch, device, a.config4_size, w, 4096)
 
     cpu = None
     if not a.no_cpu and world == 1:
@@ -473,23 +455,27 @@ def main():
         cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
                "sample": "%d of %d outer steps of sweep 1 (oracle = C restatement, bitwise the reference)"
                          % (s_cpu, n // w - 1),
-               "est_full_solve_s": dt / s_cpu * (n // w - 1) * (sum(sweeps) / len(sweeps))}
+               "est_s_per_sweep": dt / s_cpu * (n // w - 1)}
 
     line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
-            "warmup": max(3, a.warmup), "ms_per_step": ms_max / a.steps, "higher_is_better": True,
+            "warmup": W, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated on the GPU)",
-            "config": {"workload": workload_name(a), "n": n, "block_width": w, "sweeps": sweeps,
-                       "max_outer_sweeps": cap, "converged": bool(job.converged),
+            "config": {"workload": workload_name(a), "n": n, "block_width": w,
+                       "step": "one outer sweep (%d outer steps x %d block pairs) after %d warm-up sweeps"
+                               % (n // w - 1, n // w // 2, W),
                        "parallelism": ("column blocks partitioned over %d ranks (%s block exchange per step)"
                                        % (world, "NCCL" if backend == "nccl" else backend + ", host-staged"))
                        if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (F+G+Z = %.0f MB > 126 MB)" % (3 * n * n * 8 / 1e6),
-                       "wall_s_per_solve": ms_max / a.steps / 1e3},
+                       "s_per_sweep": ms_max / a.steps / 1e3},
             "roofline": roofline, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "steps": ke, "wall_s_per_solve": te / ke},
-            "gpu_launches": int(launches), "clocks": clk, "accuracy": acc, "n16384": extra}
+                    "steps": ke, "sweeps_per_call": a.e2e_sweeps,
+                    "how": "solve() on pinned numpy inputs with max_outer_sweeps=%d: copies in, sweeps, final "
+                           "rescale/unborder/sort, copies out" % a.e2e_sweeps,
+                    "wall_s_per_call": te / ke},
+            "gpu_launches": int(launches), "clocks": clk, "config4": extra}
     print(json.dumps(line), flush=True)
     if world > 1:
         barrier()

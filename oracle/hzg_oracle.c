@@ -19,6 +19,7 @@
  * zero plane too, pointwise.py:300-304).
  */
 #include <math.h>
+#include <time.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -53,6 +54,7 @@ typedef struct {
   int64_t sweeps, total, big;
   int converged;
   int fail_pair;         /* first failing pair index of the failing step, -1 */
+  double step_seconds;   /* wall time spent in outer steps (timing only, not numerics) */
 } hzo_stats;
 
 /* ------------------------------------------------------------------------ */
@@ -923,11 +925,14 @@ static int algorithm1_loop(plane_t F, plane_t G, plane_t Z, int cplx, const hzo_
   int64_t total = 0, big = 0, sweeps = 0, steps_done = 0;
   int converged = 0, status = HZO_OK;
   stats->fail_pair = -1;
+  stats->step_seconds = 0.0;
   for (int c = 0; c < sweep_cap && status == HZO_OK; ++c) {
     int64_t s_sw = 0, b_sw = 0;
     for (int step = 0; step < osteps; ++step) {
       if (step_limit >= 0 && steps_done >= step_limit) goto done;
       const int32_t* row = outer + (int64_t)step * half * 2;
+      struct timespec ts0, ts1;
+      clock_gettime(CLOCK_MONOTONIC, &ts0);
 #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
       for (int pr = 0; pr < half; ++pr) {
         int tid = 0;
@@ -938,6 +943,8 @@ static int algorithm1_loop(plane_t F, plane_t G, plane_t Z, int cplx, const hzo_
         stv[pr] = block_task(F, G, Z, cplx, row[2 * pr], row[2 * pr + 1], cfg, inner, isteps, epsn, &scr[tid],
                              &tv[pr], &bv[pr]);
       }
+      clock_gettime(CLOCK_MONOTONIC, &ts1);
+      stats->step_seconds += (double)(ts1.tv_sec - ts0.tv_sec) + 1e-9 * (double)(ts1.tv_nsec - ts0.tv_nsec);
       ++steps_done;
       for (int pr = 0; pr < half; ++pr) {
         if (stv[pr] != HZO_OK) { status = stv[pr]; stats->fail_pair = pr; break; }

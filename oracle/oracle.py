@@ -42,7 +42,7 @@ class _Cfg(ctypes.Structure):
 
 class _Stats(ctypes.Structure):
     _fields_ = [("sweeps", ctypes.c_int64), ("total", ctypes.c_int64), ("big", ctypes.c_int64),
-                ("converged", ctypes.c_int), ("fail_pair", ctypes.c_int)]
+                ("converged", ctypes.c_int), ("fail_pair", ctypes.c_int), ("step_seconds", ctypes.c_double)]
 
 
 def build():
@@ -212,7 +212,8 @@ def gsvd_blocked(Fr, Fi, Gr, Gi, cplx, cfg, threads=None, step_limit=-1, epsn=0.
                                   ctypes.byref(cfg), epsn, _p(sF), _p(sG), _p(s), ctypes.byref(st), thr,
                                   step_limit)
     return dict(status=code, U=(Fr, Fi), V=(Gr, Gi), Z=(Zr, Zi), sigmaF=sF, sigmaG=sG, sigma=s,
-                sweeps=st.sweeps, total=st.total, big=st.big, converged=bool(st.converged))
+                sweeps=st.sweeps, total=st.total, big=st.big, converged=bool(st.converged),
+                step_seconds=st.step_seconds)
 
 
 def solve(F, G, cfg=None, threads=None):
