@@ -59,9 +59,13 @@ class BlockSchedule:
     def moves(self, k):
         """Blocks changing owner between step k and step (k+1) mod steps:
         sorted list of (block, src_rank, dst_rank)."""
-        a = self.owner[k]
-        b = self.owner[(k + 1) % self.steps]
-        return [(int(blk), int(a[blk]), int(b[blk])) for blk in np.nonzero(a != b)[0]]
+        if not hasattr(self, "_moves"):
+            self._moves = {}
+        if k not in self._moves:
+            a = self.owner[k]
+            b = self.owner[(k + 1) % self.steps]
+            self._moves[k] = [(int(blk), int(a[blk]), int(b[blk])) for blk in np.nonzero(a != b)[0]]
+        return self._moves[k]
 
     def owned(self, k, rank):
         return np.nonzero(self.owner[k] == rank)[0]
@@ -145,26 +149,36 @@ def run_ranks(devs, sched, transport, cfg, allreduce=None, rescale_all=None):
     sweeps = total = big = 0
     converged = False
     for _ in range(cfg.max_outer_sweeps):
-        for k in range(sched.steps):
-            for d in devs:
-                d.run_steps(k, 1)
-            transport.exchange(sched.moves(k))
-        t = b = 0
-        for d in devs:
-            tt, bb = d.collect()
-            t += tt
-            b += bb
-        if allreduce is not None:
-            t, b = allreduce(t, b)
+        t, b = sweep_ranks(devs, sched, transport, allreduce)
         sweeps += 1
         total += t
         big += b
         if b == 0:
             converged = True
             break
+    return sweeps, total, big, converged
+
+
+def sweep_ranks(devs, sched, transport, allreduce=None):
+    """One outer sweep of the partitioned schedule: every step on every
+    rank with the block exchange after it, the counter sum, and the
+    inter-sweep Z rescale when the sweep applied big transforms
+    (blocked.py:521-542).  Returns the sweep's (total, big)."""
+    for k in range(sched.steps):
+        for d in devs:
+            d.run_steps(k, 1)
+        transport.exchange(sched.moves(k))
+    t = b = 0
+    for d in devs:
+        tt, bb = d.collect()
+        t += tt
+        b += bb
+    if allreduce is not None:
+        t, b = allreduce(t, b)
+    if b != 0:
         for d in devs:
             d.rescale_z()
-    return sweeps, total, big, converged
+    return t, b
 
 
 class PartitionedGsvd:
@@ -221,6 +235,21 @@ class PartitionedGsvd:
         self.sweeps, self.total, self.big, self.converged = run_ranks(self.devs, self.sched, self.transport, self.cfg,
                                                                       self.allreduce)
         return self
+
+    def init(self):
+        for d in self.devs:
+            d.init()
+        self.sweeps = self.total = self.big = 0
+        self.converged = False
+
+    def sweep(self):
+        """One outer sweep (after init()); returns (total, big)."""
+        t, b = sweep_ranks(self.devs, self.sched, self.transport, self.allreduce)
+        self.sweeps += 1
+        self.total += t
+        self.big += b
+        self.converged = b == 0
+        return t, b
 
     def finalize(self, n0=None, mF0=None, mG0=None, sort=True):
         self.transport.exchange(gather_blocks(self.sched))

@@ -12,7 +12,10 @@ output.
 """
 
 import ctypes
+import dataclasses
 import math
+import os
+import threading
 
 import numpy as np
 
@@ -182,16 +185,18 @@ def _planes_of(m):
     return m.re, (m.im if m.is_complex else None)
 
 
-def upload_bordered(F, G, w, device=None, torch=None):
+def upload_bordered(F, G, w, device=None, torch=None, out=None):
     """Copy (F, G) to the GPU and border them there exactly like
     border_pair(p, 2w, 2w) (core.py:186-218): pad columns carry a single 1
-    on the extended diagonal, pad rows are zero."""
+    on the extended diagonal, pad rows are zero.  ``out``: planes of the
+    same bordered shape to fill instead of allocating."""
     torch = torch or _torch()
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     n0 = F.cols
     padF, mF = bordered_shape(n0, F.rows, 2 * w, 2 * w)
     padG, mG = bordered_shape(n0, G.rows, 2 * w, 2 * w)
     n = n0 + padF
+    dst = out
     out = {}
     for key, M, m in (("F", F, mF), ("G", G, mG)):
         re, im = _planes_of(M)
@@ -199,7 +204,12 @@ def upload_bordered(F, G, w, device=None, torch=None):
             if host is None:
                 out[key + suffix] = None
                 continue
-            d = torch.zeros((n, m), dtype=torch.float64, device=dev)
+            if dst is not None:
+                d = dst[key + suffix]
+                if n0 < n or M.rows < m:
+                    d.zero_()
+            else:
+                d = torch.zeros((n, m), dtype=torch.float64, device=dev)
             h = torch.from_numpy(np.asfortranarray(host).T)
             d[:n0, :M.rows].copy_(h, non_blocking=True)
             if suffix == "r" and padF:
@@ -288,11 +298,40 @@ def solve(F, G, cfg=None, workers=1, worker_sweeps=1):
         from .dist import solve_blocks
         return solve_blocks(F, G, cfg, workers)
     p = ProblemPair(F, G)
-    planes, n, mF, mG = upload_bordered(p.F, p.G, cfg.block_width)
-    dev = DeviceGsvd(planes, cfg)
-    try:
+    with _cache_lock:
+        dev = _cached_solver(p, cfg)
         dev.run()
         out = dev.finalize(p.n, p.F.rows, p.G.rows, sort=True)
         return _result_from_device(dev, out, p.is_complex, workers)
-    finally:
+
+
+# The last solve's device context (planes, workspace, captured sweep graph)
+# is kept for the next solve of the same shape and configuration: the graph
+# is captured once instead of per call.
+_cache_lock = threading.Lock()
+_cache = {"key": None, "dev": None}
+
+
+def _cached_solver(p, cfg):
+    torch = _torch()
+    w = cfg.block_width
+    # the HZG_* tuning variables shape the context too
+    knobs = tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("HZG_")))
+    key = (torch.cuda.current_device(), p.n, p.F.rows, p.G.rows, p.is_complex, dataclasses.astuple(cfg), knobs)
+    if _cache["key"] == key:
+        dev = _cache["dev"]
+        upload_bordered(p.F, p.G, w, out=dev.planes)
+        return dev
+    clear_cache()
+    planes, n, mF, mG = upload_bordered(p.F, p.G, w)
+    dev = DeviceGsvd(planes, cfg)
+    _cache["key"], _cache["dev"] = key, dev
+    return dev
+
+
+def clear_cache():
+    """Release the device context kept by solve()."""
+    dev = _cache["dev"]
+    _cache["key"], _cache["dev"] = None, None
+    if dev is not None:
         dev.close()
