@@ -292,6 +292,8 @@ def solve(F, G, cfg=None, workers=1, worker_sweeps=1):
         G = MatrixPlanePair.from_dense(G)
     if workers < 1:
         raise ValueError("need at least one worker")
+    _torch()  # no device or no libhzg.so: fail loudly, also for the 1x1 closed form
+    _native.load()
     if F.cols == 1:
         return gsvd_1x1(F, G)
     if workers > 1:

@@ -1,9 +1,7 @@
 out=gpurun_out
 tag=${1:-x}
-HZG_SPLIT_ROWS=256 timeout 900 python -m pytest tests -m gpu -x -q -k "fused" > $out/${tag}_pytest_fused.log 2>&1; echo "rc $?" >> $out/${tag}_pytest_fused.log
-echo "fused split 256" >> $out/${tag}_explore.txt
-HZG_SPLIT_ROWS=256 timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
-echo "unfused split 256" >> $out/${tag}_explore.txt
-HZG_SPLIT_ROWS=256 HZG_FUSED=0 timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
-echo "unfused split 512" >> $out/${tag}_explore.txt
-HZG_FUSED=0 timeout 900 python tools/explore.py 16384 gauss 16 fb 2 >> $out/${tag}_explore.txt 2>&1
+for pc in 1024 512 256; do for sr in 0 256; do
+  echo "post chunk $pc split rows $sr" >> $out/${tag}_explore.txt
+  if [ $sr = 0 ]; then HZG_POST_CHUNK=$pc timeout 900 python tools/explore.py 4096 cond 16 fb 100 >> $out/${tag}_explore.txt 2>&1;
+  else HZG_SPLIT_ROWS=$sr HZG_POST_CHUNK=$pc timeout 900 python tools/explore.py 4096 cond 16 fb 100 >> $out/${tag}_explore.txt 2>&1; fi
+done; done
