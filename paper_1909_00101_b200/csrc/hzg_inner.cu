@@ -991,7 +991,31 @@ int launch_inner_g(const InnerParams& p, cudaStream_t s) {
     cap = e ? std::max(0, std::atoi(e)) : 0;
   }
   const int grid = cap > 0 && cap < p.sp.pn ? cap : p.sp.pn;
-  k_inner<TW, CPLX, SWZ><<<grid, InnerGeo<TW, CPLX>::NW * 32, smem, s>>>(p);
+  // HZG_INNER_PRIO=1 launches the inner solves at the highest scheduling
+  // priority (a node attribute inside the sweep graph), so their latency-
+  // bound CTAs are placed ahead of queued streaming CTAs (for tuning)
+  static int prio = -1;
+  if (prio < 0) {
+    const char* e = std::getenv("HZG_INNER_PRIO");
+    prio = e ? std::atoi(e) : 0;
+  }
+  if (prio) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(InnerGeo<TW, CPLX>::NW * 32);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributePriority;
+    at[0].val.priority = hi;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, k_inner<TW, CPLX, SWZ>, p);
+  } else {
+    k_inner<TW, CPLX, SWZ><<<grid, InnerGeo<TW, CPLX>::NW * 32, smem, s>>>(p);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 

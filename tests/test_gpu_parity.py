@@ -345,3 +345,51 @@ def test_wavefront_groups_bitwise_invariant(monkeypatch):
         assert (r.sweeps, r.total_transforms, r.big_transforms) == \
             (runs[0].sweeps, runs[0].total_transforms, runs[0].big_transforms)
         assert np.array_equal(r.sigma, runs[0].sigma) and np.array_equal(r.Z.re, runs[0].Z.re)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_pivot_property_many_random_2x2(cplx):
+    """The 2x2 Hari-Zimmermann transform on the device (2w = 2: one pivot per
+    block) on many random pivots, including nearly parallel G columns and
+    tiny / huge scalings: bitwise the oracle's transform, counters included
+    (the reference's kernel property suites, test_acceptance.py:267-290,
+    test_kernel2x2.py:167-203)."""
+    rng = np.random.default_rng(2024 + cplx)
+    cfg = hz.SolverConfig(block_width=1)
+    epsn = EPS * np.sqrt(64.0)
+    for t in range(400):
+        m = 3
+        Y = rng.standard_normal((m, 2)) + (1j * rng.standard_normal((m, 2)) if cplx else 0)
+        X = rng.standard_normal((m, 2)) + (1j * rng.standard_normal((m, 2)) if cplx else 0)
+        if t % 4 == 1:  # nearly parallel G columns
+            X[:, 1] = X[:, 0] + 1e-7 * X[:, 1]
+        if t % 4 == 2:  # badly scaled
+            Y = Y * 10.0 ** rng.integers(-150, 150)
+            X[:, 0] = X[:, 0] * 10.0 ** rng.integers(-8, 8)
+        grams = []
+        for M in (Y, X):
+            Ar, Ai = O.grammian(np.asfortranarray(M.real), np.asfortranarray(M.imag) if cplx else None, 0, 1, 1,
+                                cplx)
+            grams.append((Ar, Ai))
+        (Fr, Fi), (Gr, Gi) = grams
+        Fh, st1 = O.cholesky_upper(Fr + 1j * Fi if cplx else Fr)
+        Gh, st2 = O.cholesky_upper(Gr + 1j * Gi if cplx else Gr)
+        if st1 or st2:
+            continue
+        _, _, Zo, tot, big, st = O.block_inner(Fh, Gh, O.cfg_from(cfg), epsn)
+        Zg, cnt = _gpu_block(2, cplx, cfg, epsn, grams)
+        assert cnt[2] == st and (cnt[0], cnt[1]) == (tot, big)
+        assert np.array_equal(Zg, Zo), t
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_sigma_vs_numpy_svd_of_F_Ginv(cplx):
+    """sigma against numpy's SVD of F G^-1 at n = 24 (test_blocked.py:263-273),
+    with the reference's tolerance 1e-10."""
+    rng = np.random.default_rng(24 + cplx)
+    n = 24
+    F = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)
+    G = rng.standard_normal((n, n)) + (1j * rng.standard_normal((n, n)) if cplx else 0)
+    r = hz.solve(F, G, hz.SolverConfig(block_width=4))
+    ref = np.linalg.svd(F @ np.linalg.inv(G), compute_uv=False)
+    assert np.max(np.abs(np.sort(r.sigma)[::-1] - ref) / ref) <= 1e-10
