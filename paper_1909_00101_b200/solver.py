@@ -219,9 +219,14 @@ def upload_bordered(F, G, w, device=None, torch=None, out=None):
     return out, n, mF, mG
 
 
-def _to_numpy_plane(t):
-    """(cols, rows) device tensor -> Fortran (rows, cols) numpy plane."""
-    return t.cpu().numpy().T
+def _to_host(t):
+    """Start the copy of a device tensor into pinned host memory (torch's
+    caching host allocator: blocks freed with the caller's arrays are reused
+    by the next solve).  Synchronize before reading."""
+    torch = _torch()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    return h
 
 
 def gsvd_1x1(F, G):
@@ -245,13 +250,16 @@ def gsvd_1x1(F, G):
 
 
 def _result_from_device(dev, out, cplx, workers=1):
+    host = {k: _to_host(v) for k, v in out.items() if v is not None}
+    _torch().cuda.current_stream().synchronize()
+
     def plane(kr, ki):
-        re = _to_numpy_plane(out[kr])
-        im = _to_numpy_plane(out[ki]) if cplx else None
+        re = host[kr].numpy().T
+        im = host[ki].numpy().T if cplx else None
         return MatrixPlanePair(re.shape[0], re.shape[1], re, im, cplx)
 
-    return GsvdResult(plane("Ur", "Ui"), plane("Vr", "Vi"), plane("Zr", "Zi"), out["sigmaF"].cpu().numpy(),
-                      out["sigmaG"].cpu().numpy(), out["sigma"].cpu().numpy(), sweeps=dev.sweeps,
+    return GsvdResult(plane("Ur", "Ui"), plane("Vr", "Vi"), plane("Zr", "Zi"), host["sigmaF"].numpy(),
+                      host["sigmaG"].numpy(), host["sigma"].numpy(), sweeps=dev.sweeps,
                       total_transforms=dev.total, big_transforms=dev.big, converged=dev.converged,
                       workers=workers)
 
