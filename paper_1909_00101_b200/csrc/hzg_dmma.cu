@@ -45,21 +45,6 @@ __device__ __forceinline__ void issue_tile_load(const Plane& Y, const int32_t* c
   }
 }
 
-// ---------------------------------------------------------------------------
-// Grammian partials.  Warp (bi, bj), bi <= bj, owns the 16x16 block of the
-// upper triangle made of 8x8 tiles (2bi..2bi+1, 2bj..2bj+1); diagonal
-// blocks skip their strictly-lower tile.
-// ---------------------------------------------------------------------------
-template <int TW, bool CPLX>
-struct GramCfg {
-  static constexpr int NB = TW / 16;
-  static constexpr int NWARP = NB * (NB + 1) / 2;
-  static constexpr int NP = CPLX ? 2 : 1;
-  static constexpr int NS = 4;
-  static constexpr size_t STAGE = (size_t)NP * TW * kRS;  // doubles
-  static constexpr size_t SMEM = NS * STAGE * sizeof(double) + 64;
-};
-
 struct GramParams {
   Plane Y[2];
   StepPairs sp;
@@ -68,149 +53,9 @@ struct GramParams {
   const int32_t* plist;  // optional: the pairs of this launch (blockIdx.x indexes it)
 };
 
-template <int TW, bool CPLX>
-__global__ void __launch_bounds__(GramCfg<TW, CPLX>::NWARP * 32) k_gram_dmma(GramParams P) {
-  using C = GramCfg<TW, CPLX>;
-  constexpr int NP = C::NP;
-  constexpr int w = TW / 2;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* stages = reinterpret_cast<double*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::NS * C::STAGE * sizeof(double));
-
-  const int pair = P.plist ? P.plist[blockIdx.x] : P.sp.p0 + blockIdx.x;
-  const int mat = blockIdx.y, split = blockIdx.z;
-  if (split >= P.gw.nsplit[mat]) return;
-  const Plane& Y = P.Y[mat];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
-  const int64_t L = P.gw.chunk[mat];
-  const int64_t rbeg = (int64_t)split * L;
-  const int64_t rend = rbeg + L < Y.rows ? rbeg + L : Y.rows;
-  const int ntiles = rend > rbeg ? (int)((rend - rbeg + kR - 1) / kR) : 0;
-
-  // warp -> (bi, bj)
-  int bi = 0, bj = 0;
-  {
-    int q = warp;
-    while (q >= C::NB - bi) {
-      q -= C::NB - bi;
-      ++bi;
-    }
-    bj = bi + q;
-  }
-  const bool diag = bi == bj;
-
-  if (tid == 0) {
-    for (int s = 0; s < C::NS; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0)
-    for (int s = 0; s < C::NS && s < ntiles; ++s) {
-      int64_t r0 = rbeg + (int64_t)s * kR;
-      int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
-      issue_tile_load<TW, NP>(Y, cp, r0, nv, stages + s * C::STAGE, &full[s], lane);
-    }
-
-  // accumulators: tile (ii, jj) of the block, ii, jj in {0, 1}; [plane][tile][2]
-  double acc[NP][4][2];
-#pragma unroll
-  for (int p = 0; p < NP; ++p)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[p][q][0] = acc[p][q][1] = 0.0;
-
-  for (int it = 0; it < ntiles; ++it) {
-    const int s = it % C::NS;
-    mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
-    const double* st = stages + s * C::STAGE;
-    const int64_t r0 = rbeg + (int64_t)it * kR;
-    const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
-    // column offsets of this lane's fragment columns
-    const double* ar0 = st + (size_t)(bi * 16 + g) * kRS;
-    const double* ar1 = st + (size_t)(bi * 16 + 8 + g) * kRS;
-    const double* br0 = st + (size_t)(bj * 16 + g) * kRS;
-    const double* br1 = st + (size_t)(bj * 16 + 8 + g) * kRS;
-#pragma unroll 4
-    for (int ks = 0; ks < kR / 4; ++ks) {
-      const int k = ks * 4 + t;
-      const bool ok = k < nv;
-      double a0 = ok ? ar0[k] : 0.0, a1 = ok ? ar1[k] : 0.0;
-      double b0 = diag ? a0 : (ok ? br0[k] : 0.0);
-      double b1 = diag ? a1 : (ok ? br1[k] : 0.0);
-      if (!CPLX) {
-        dmma884(acc[0][0][0], acc[0][0][1], a0, b0);
-        dmma884(acc[0][1][0], acc[0][1][1], a0, b1);
-        if (!diag) dmma884(acc[0][2][0], acc[0][2][1], a1, b0);
-        dmma884(acc[0][3][0], acc[0][3][1], a1, b1);
-      } else {
-        const size_t IM = (size_t)TW * kRS;
-        double c0 = ok ? ar0[IM + k] : 0.0, c1 = ok ? ar1[IM + k] : 0.0;  // imag of the a columns
-        double d0 = diag ? c0 : (ok ? br0[IM + k] : 0.0);
-        double d1 = diag ? c1 : (ok ? br1[IM + k] : 0.0);
-        // Re += ar*br + ai*bi ; Im += ar*bi - ai*br
-        dmma884(acc[0][0][0], acc[0][0][1], a0, b0);
-        dmma884(acc[0][0][0], acc[0][0][1], c0, d0);
-        dmma884(acc[1][0][0], acc[1][0][1], a0, d0);
-        dmma884(acc[1][0][0], acc[1][0][1], -c0, b0);
-        dmma884(acc[0][1][0], acc[0][1][1], a0, b1);
-        dmma884(acc[0][1][0], acc[0][1][1], c0, d1);
-        dmma884(acc[1][1][0], acc[1][1][1], a0, d1);
-        dmma884(acc[1][1][0], acc[1][1][1], -c0, b1);
-        if (!diag) {
-          dmma884(acc[0][2][0], acc[0][2][1], a1, b0);
-          dmma884(acc[0][2][0], acc[0][2][1], c1, d0);
-          dmma884(acc[1][2][0], acc[1][2][1], a1, d0);
-          dmma884(acc[1][2][0], acc[1][2][1], -c1, b0);
-        }
-        dmma884(acc[0][3][0], acc[0][3][1], a1, b1);
-        dmma884(acc[0][3][0], acc[0][3][1], c1, d1);
-        dmma884(acc[1][3][0], acc[1][3][1], a1, d1);
-        dmma884(acc[1][3][0], acc[1][3][1], -c1, b1);
-      }
-    }
-    __syncthreads();
-    if (warp == 0 && it + C::NS < ntiles) {
-      int64_t r1 = rbeg + (int64_t)(it + C::NS) * kR;
-      int nv1 = (int)(rend - r1 < kR ? rend - r1 : kR);
-      issue_tile_load<TW, NP>(Y, cp, r1, nv1, stages + s * C::STAGE, &full[s], lane);
-    }
-  }
-
-  // write the upper tiles: element (r, c) at c*TW + r
-  double* out = P.gw.part + (((int64_t)pair * 2 + mat) * P.gw.smax + split) * NP * TW * TW;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int ii = q >> 1, jj = q & 1;
-    if (diag && ii > jj) continue;
-    const int r = bi * 16 + ii * 8 + g;
-    const int c = bj * 16 + jj * 8 + 2 * t;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      out[(size_t)p * TW * TW + (size_t)c * TW + r] = acc[p][q][0];
-      out[(size_t)p * TW * TW + (size_t)(c + 1) * TW + r] = acc[p][q][1];
-    }
-  }
-  (void)w;
-}
-
 // ---------------------------------------------------------------------------
-// Postmultiply [Y_p Y_q] <- [Y_p Y_q] Z~ for F, G and Z.  4 warps along the
-// 64 rows (16 rows each) x WN warps along the columns (32 columns each).
+// Postmultiply [Y_p Y_q] <- [Y_p Y_q] Z~ for F, G and Z (k_post_ws below).
 // ---------------------------------------------------------------------------
-template <int TW, bool CPLX>
-struct PostCfg {
-  static constexpr int NP = CPLX ? 2 : 1;
-  static constexpr int NT_N = TW / 8;                 // 8-col tiles
-  static constexpr int WN = NT_N > 4 ? NT_N / 4 : 1;  // warps along N
-  static constexpr int TN = NT_N / WN;                // tiles per warp along N
-  static constexpr int NWARP = 4 * WN;
-  static constexpr int NS = (CPLX || TW > 32) ? 2 : 3;
-  static constexpr int ZS = TW + 4;  // padded stride of Z~ (column-major)
-  static constexpr size_t STAGE = (size_t)NP * TW * kRS;
-  static constexpr size_t SMEM = (NS * STAGE + (size_t)NP * TW * ZS) * sizeof(double) + 64;
-};
-
 struct PostParams {
   Plane Y[3];
   StepPairs sp;
@@ -220,129 +65,8 @@ struct PostParams {
   int mat0;       // first matrix of the launch (blockIdx.y + mat0: 0 F, 1 G, 2 Z)
 };
 
-template <int TW, bool CPLX>
-__global__ void __launch_bounds__(PostCfg<TW, CPLX>::NWARP * 32) k_post_dmma(PostParams P) {
-  using C = PostCfg<TW, CPLX>;
-  constexpr int NP = C::NP;
-  constexpr int w = TW / 2;
-  const int pair = P.sp.p0 + blockIdx.x, mat = blockIdx.y + P.mat0;
-  if (P.io.ident[pair]) return;
-  const Plane& Y = P.Y[mat];
-  const int64_t rbeg = (int64_t)blockIdx.z * P.chunk;
-  if (rbeg >= Y.rows) return;
-  const int64_t rend = rbeg + P.chunk < Y.rows ? rbeg + P.chunk : Y.rows;
-  const int ntiles = (int)((rend - rbeg + kR - 1) / kR);
-
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* stages = reinterpret_cast<double*>(smem_raw);
-  double* zs = stages + C::NS * C::STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(zs + (size_t)NP * TW * C::ZS);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp % 4, wn = warp / 4;
-  const int32_t* cp = P.sp.colpair + ((int64_t)P.step * P.sp.npairs + pair) * 2;
-
-  if (tid == 0) {
-    for (int s = 0; s < C::NS; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == 0)
-    for (int s = 0; s < C::NS && s < ntiles; ++s) {
-      int64_t r0 = rbeg + (int64_t)s * kR;
-      int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
-      issue_tile_load<TW, NP>(Y, cp, r0, nv, stages + s * C::STAGE, &full[s], lane);
-    }
-  // Z~ (column-major TW x TW per plane) -> padded shared copy
-  const double* zsrc = P.io.zt + (int64_t)pair * NP * TW * TW;
-  for (int e = tid; e < NP * TW * TW; e += blockDim.x) {
-    int p = e / (TW * TW), r = e % TW, c = (e / TW) % TW;
-    zs[(size_t)p * TW * C::ZS + (size_t)c * C::ZS + r] = zsrc[e];
-  }
-  __syncthreads();
-
-  for (int it = 0; it < ntiles; ++it) {
-    const int s = it % C::NS;
-    mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
-    double* st = stages + s * C::STAGE;
-    const int64_t r0 = rbeg + (int64_t)it * kR;
-    const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
-
-    double acc[NP][2][C::TN][2];
-#pragma unroll
-    for (int p = 0; p < NP; ++p)
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < C::TN; ++ni) acc[p][mi][ni][0] = acc[p][mi][ni][1] = 0.0;
-
-#pragma unroll 2
-    for (int ks = 0; ks < TW / 4; ++ks) {
-      const int k = ks * 4 + t;  // inner index = column of Y, row of Z~
-      double ar[2], ai[2];
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const int row = wm * 16 + mi * 8 + g;
-        ar[mi] = st[(size_t)k * kRS + row];
-        ai[mi] = CPLX ? st[(size_t)(TW + k) * kRS + row] : 0.0;
-      }
-#pragma unroll
-      for (int ni = 0; ni < C::TN; ++ni) {
-        const int col = (wn * C::TN + ni) * 8 + g;
-        const double zr = zs[(size_t)col * C::ZS + k];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi) dmma884(acc[0][mi][ni][0], acc[0][mi][ni][1], ar[mi], zr);
-        if (CPLX) {
-          const double zi = zs[(size_t)TW * C::ZS + (size_t)col * C::ZS + k];
-#pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
-            dmma884(acc[0][mi][ni][0], acc[0][mi][ni][1], -ai[mi], zi);
-            dmma884(acc[NP - 1][mi][ni][0], acc[NP - 1][mi][ni][1], ar[mi], zi);
-            dmma884(acc[NP - 1][mi][ni][0], acc[NP - 1][mi][ni][1], ai[mi], zr);
-          }
-        }
-      }
-    }
-    __syncthreads();  // every warp has read the whole tile
-#pragma unroll
-    for (int p = 0; p < NP; ++p)
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < C::TN; ++ni) {
-          const int row = wm * 16 + mi * 8 + g;
-          const int col = (wn * C::TN + ni) * 8 + 2 * t;
-          st[(size_t)(p * TW + col) * kRS + row] = acc[p][mi][ni][0];
-          st[(size_t)(p * TW + col + 1) * kRS + row] = acc[p][mi][ni][1];
-        }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t bytes = (uint32_t)nv * 8u;
-      for (int q = lane; q < TW * NP; q += 32) {
-        const int c = q % TW, pl = q / TW;
-        double* base = pl == 0 ? Y.re : Y.im;
-        bulk_s2g(base + pair_col(cp, w, c) * Y.ld + r0, st + (size_t)q * kRS, bytes);
-      }
-      bulk_commit();
-      // refill the stage drained one iteration ago: its bulk store has had a
-      // whole tile of compute to finish reading shared memory
-      if (it >= 1 && it - 1 + C::NS < ntiles) {
-        bulk_wait_read<1>();
-        __syncwarp();
-        const int sp = (it - 1) % C::NS;
-        int64_t r1 = rbeg + (int64_t)(it - 1 + C::NS) * kR;
-        int nv1 = (int)(rend - r1 < kR ? rend - r1 : kR);
-        issue_tile_load<TW, NP>(Y, cp, r1, nv1, stages + sp * C::STAGE, &full[sp], lane);
-      }
-    }
-  }
-  if (warp == 0) bulk_wait_all<0>();
-}
-
 // ---------------------------------------------------------------------------
-// Warp-specialized streaming kernels (2w <= 32): warp 4 is the TMA producer
+// Warp-specialized streaming kernels (2w = 16, 32, 64): warp 4 is the TMA producer
 // (bulk loads, and for the postmultiply the bulk stores), warps 0-3 compute.
 // Stages are handed over with mbarriers only -- no CTA-wide barrier inside
 // the tile loop -- so DMMA work, loads and stores of different tiles overlap.
@@ -354,7 +78,7 @@ struct GramWsCfg {
   static constexpr int NT = TW / 8;
   static constexpr int NTILE = NT * (NT + 1) / 2;
   static constexpr int NP = CPLX ? 2 : 1;
-  static constexpr int NS = 4;
+  static constexpr int NS = TW <= 32 ? 4 : (CPLX ? 2 : 3);  // stages within 227 KB
   static constexpr int KSTRIDE = CPLX ? 2 : 4;
   static constexpr size_t STAGE = (size_t)NP * TW * kRS;
   static constexpr size_t RED = (size_t)4 * NTILE * 64;
@@ -470,7 +194,7 @@ template <int TW, bool CPLX>
 struct PostWsCfg {
   static constexpr int NP = CPLX ? 2 : 1;
   static constexpr int TN = TW / 8;  // 8-column tiles, all in one warp
-  static constexpr int NS = CPLX ? 2 : 3;
+  static constexpr int NS = (CPLX || TW > 32) ? 2 : 3;  // 2w = 64 real: 2 CTAs per SM
   static constexpr int ZS = TW + 4;
   static constexpr size_t STAGE = (size_t)NP * TW * kRS;
   static constexpr size_t SMEM = (NS * STAGE + (size_t)NP * TW * ZS) * sizeof(double) + 2 * NS * 8 + 64;
@@ -829,19 +553,6 @@ void set_smem(K k, size_t bytes) {
 }
 
 template <int TW, bool CPLX>
-int gram_t(const GramParams& p, cudaStream_t s) {
-  using C = GramCfg<TW, CPLX>;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_gram_dmma<TW, CPLX>, C::SMEM);
-    once = true;
-  }
-  dim3 grid(p.sp.pn, 2, p.gw.smax);
-  k_gram_dmma<TW, CPLX><<<grid, C::NWARP * 32, C::SMEM, s>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
-}
-
-template <int TW, bool CPLX>
 int gram_ws_t(const GramParams& p, cudaStream_t s) {
   using C = GramWsCfg<TW, CPLX>;
   static bool once = false;
@@ -864,19 +575,6 @@ int post_ws_t(const PostParams& p, int64_t mmax, int nmats, cudaStream_t s) {
   }
   dim3 grid(p.sp.pn, nmats, (unsigned)((mmax + p.chunk - 1) / p.chunk));
   k_post_ws<TW, CPLX><<<grid, 160, C::SMEM, s>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : 3;
-}
-
-template <int TW, bool CPLX>
-int post_t(const PostParams& p, int64_t mmax, int nmats, cudaStream_t s) {
-  using C = PostCfg<TW, CPLX>;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_post_dmma<TW, CPLX>, C::SMEM);
-    once = true;
-  }
-  dim3 grid(p.sp.pn, nmats, (unsigned)((mmax + p.chunk - 1) / p.chunk));
-  k_post_dmma<TW, CPLX><<<grid, C::NWARP * 32, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
@@ -913,7 +611,7 @@ int launch_gram_dmma(const Plane& F, const Plane& G, const StepPairs& sp, int st
     case 32:
       return cplx ? gram_ws_t<32, true>(p, s) : gram_ws_t<32, false>(p, s);
     case 64:
-      return cplx ? gram_t<64, true>(p, s) : gram_t<64, false>(p, s);
+      return cplx ? gram_ws_t<64, true>(p, s) : gram_ws_t<64, false>(p, s);
   }
   return 4;
 }
@@ -933,8 +631,7 @@ int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const S
     case 32:
       return cplx ? post_ws_t<32, true>(p, mmax, nmats, s) : post_ws_t<32, false>(p, mmax, nmats, s);
     case 64:
-      p.chunk = 512;
-      return cplx ? post_t<64, true>(p, mmax, nmats, s) : post_t<64, false>(p, mmax, nmats, s);
+      return cplx ? post_ws_t<64, true>(p, mmax, nmats, s) : post_ws_t<64, false>(p, mmax, nmats, s);
   }
   return 4;
 }

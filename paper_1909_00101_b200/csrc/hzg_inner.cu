@@ -36,14 +36,14 @@ template <int TW, bool CPLX>
 struct InnerGeo {
   static constexpr int NPIV = TW / 2;  // pivots per inner step
   static constexpr int LT = TW <= 2 ? 2 : (TW <= 4 ? 4 : (TW <= 8 ? 8 : (TW <= 16 ? 16 : (TW <= 32 ? 32 : 64))));
-  static constexpr int RPL = LT >= 4 ? 4 : LT;  // rows per lane
+  static constexpr int RPL = (TW == 64 && !CPLX) ? 8 : (LT >= 4 ? 4 : LT);  // rows per lane
   static constexpr int LP = LT / RPL;           // lanes per pivot
   static constexpr int LV = LP == 1 ? 0 : (LP == 2 ? 1 : (LP == 4 ? 2 : (LP == 8 ? 3 : 4)));
   static constexpr int PG = 32 / LP;            // pivots per warp
   static constexpr int NW = (NPIV + PG - 1) / PG;
   static constexpr int HL = LV < 3 ? LV : 3;    // halving levels over the 8 quantities
   static constexpr int R = 8 >> HL;             // quantities per lane after halving
-  static constexpr bool VEC = TW % 4 == 0 && RPL == 4;  // 16-byte shared loads / stores
+  static constexpr bool VEC = TW % 4 == 0 && RPL >= 4 && TW % RPL == 0;  // 16-byte shared loads / stores
   static constexpr int NCB = NPIV > NW ? NPIV : NW;     // compensated-variant scratch slots
 };
 
@@ -126,26 +126,27 @@ struct HalvingTree {
   }
 };
 
-// Shared-memory row order of the 2w x 2w factors.  With SWZ, the rows of
-// every column are stored as [rows 4l, 4l+1 for l = 0..][rows 4l+2, 4l+3 for
-// l = 0..], so the 16-byte loads of the 8 lanes that share a column (each
-// holding rows 4l .. 4l+3) cover 128 contiguous bytes per instruction --
-// conflict-free -- while each lane still owns an aligned 4-row block of the
-// reference tree.
-template <bool SWZ, int TW>
+// Shared-memory row order of the 2w x 2w factors.  With a swizzle period
+// SW (= the rows per lane of the pointwise loop, 4 or 8), the rows of every
+// column are stored as [rows SW*l, SW*l+1 for l = 0..][rows SW*l+2,
+// SW*l+3 ..]..., so the 16-byte loads of the lanes that share a column
+// (each holding the aligned block of rows SW*l .. SW*l+SW-1) cover 128
+// contiguous bytes per instruction -- conflict-free -- while each lane still
+// owns an aligned block of the reference tree.  SW = 0: natural order.
+template <int SW, int TW>
 __device__ __forceinline__ int rp(int r) {
-  if constexpr (SWZ) {
-    return ((r >> 1) & 1) * (TW / 2) + ((r >> 2) << 1) + (r & 1);
+  if constexpr (SW > 0) {
+    return ((r % SW) >> 1) * (2 * TW / SW) + ((r / SW) << 1) + (r & 1);
   } else {
     return r;
   }
 }
 
-template <bool SWZ, int TW>
+template <int SW, int TW>
 __device__ __forceinline__ int rp_inv(int q) {
-  if constexpr (SWZ) {
-    const int h = q / (TW / 2), rem = q % (TW / 2);
-    return ((rem >> 1) << 2) + 2 * h + (rem & 1);
+  if constexpr (SW > 0) {
+    const int e = q / (2 * TW / SW), rem = q % (2 * TW / SW);
+    return (rem >> 1) * SW + 2 * e + (rem & 1);
   } else {
     return q;
   }
@@ -153,15 +154,15 @@ __device__ __forceinline__ int rp_inv(int q) {
 
 // Rows r0 .. r0+RPL-1 of column `col` of a TW x TW column-major matrix
 // (zeros beyond TW, like the reference's tree padding).
-template <int TW, bool VEC, int RPL, bool SWZ = false>
+template <int TW, bool VEC, int RPL, int SW = 0>
 __device__ __forceinline__ void load_rows(const double* m, int col, int r0, double (&x)[RPL]) {
   if constexpr (VEC) {
     if (r0 < TW) {
-      // halves: rows r0, r0+1 and r0+2, r0+3 (adjacent, or TW/2 apart when swizzled)
-      const double* b = m + col * TW + (SWZ ? r0 / 2 : r0);
+      // row pairs r0+2e, r0+2e+1 (adjacent, or 2 TW / SW apart when swizzled)
+      const double* b = m + col * TW + (SW ? 2 * (r0 / RPL) : r0);
 #pragma unroll
       for (int e = 0; e < RPL / 2; ++e) {
-        const double2 d = *reinterpret_cast<const double2*>(b + e * (SWZ ? TW / 2 : 2));
+        const double2 d = *reinterpret_cast<const double2*>(b + e * (SW ? 2 * TW / SW : 2));
         x[2 * e] = d.x;
         x[2 * e + 1] = d.y;
       }
@@ -175,14 +176,14 @@ __device__ __forceinline__ void load_rows(const double* m, int col, int r0, doub
   }
 }
 
-template <int TW, bool VEC, int RPL, bool SWZ = false>
+template <int TW, bool VEC, int RPL, int SW = 0>
 __device__ __forceinline__ void store_rows(double* m, int col, int r0, const double (&x)[RPL]) {
   if constexpr (VEC) {
     if (r0 < TW) {
-      double* b = m + col * TW + (SWZ ? r0 / 2 : r0);
+      double* b = m + col * TW + (SW ? 2 * (r0 / RPL) : r0);
 #pragma unroll
       for (int e = 0; e < RPL / 2; ++e)
-        *reinterpret_cast<double2*>(b + e * (SWZ ? TW / 2 : 2)) = make_double2(x[2 * e], x[2 * e + 1]);
+        *reinterpret_cast<double2*>(b + e * (SW ? 2 * TW / SW : 2)) = make_double2(x[2 * e], x[2 * e + 1]);
     }
   } else {
 #pragma unroll
@@ -199,12 +200,14 @@ __device__ __forceinline__ double row_tree(const double (&x)[RPL]) {
     return x[0];
   } else if constexpr (RPL == 2) {
     return x[0] + x[1];
-  } else {
+  } else if constexpr (RPL == 4) {
     return (x[0] + x[1]) + (x[2] + x[3]);
+  } else {
+    return ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
   }
 }
 
-template <int TW, bool CPLX, bool SWZ = false>
+template <int TW, bool CPLX, int SW = 0>
 __device__ __forceinline__ void load_col(const double* __restrict__ re, const double* __restrict__ im, int col,
                                          int lane, double (&r)[Lanes<TW>::EPL], double (&i)[Lanes<TW>::EPL]) {
   constexpr int EPL = Lanes<TW>::EPL;
@@ -212,13 +215,13 @@ __device__ __forceinline__ void load_col(const double* __restrict__ re, const do
   for (int e = 0; e < EPL; ++e) {
     int row = lane * EPL + e;
     bool ok = row < TW;
-    const int q = ok ? rp<SWZ, TW>(row) : 0;
+    const int q = ok ? rp<SW, TW>(row) : 0;
     r[e] = ok ? re[col * TW + q] : 0.0;
     i[e] = (CPLX && ok) ? im[col * TW + q] : 0.0;
   }
 }
 
-template <int TW, bool CPLX, bool SWZ = false>
+template <int TW, bool CPLX, int SW = 0>
 __device__ __forceinline__ void store_col(double* re, double* im, int col, int lane,
                                           const double (&r)[Lanes<TW>::EPL], const double (&i)[Lanes<TW>::EPL]) {
   constexpr int EPL = Lanes<TW>::EPL;
@@ -226,7 +229,7 @@ __device__ __forceinline__ void store_col(double* re, double* im, int col, int l
   for (int e = 0; e < EPL; ++e) {
     int row = lane * EPL + e;
     if (row < TW) {
-      const int q = rp<SWZ, TW>(row);
+      const int q = rp<SW, TW>(row);
       re[col * TW + q] = r[e];
       if (CPLX) im[col * TW + q] = i[e];
     }
@@ -249,10 +252,10 @@ __device__ __forceinline__ double dot_im_term(double ar, double ai, double br, d
 
 // Column-oriented Cholesky of a Hermitian TW x TW matrix by one warp, in the
 // exact operation order of blocked.py:59-94 (lane x owns row x).
-template <int TW, bool CPLX, bool SWZ>
+template <int TW, bool CPLX, int SW>
 __device__ int warp_cholesky(double* Ar, double* Ai, int lane) {
-#define A_(x, y) Ar[(y) * TW + rp<SWZ, TW>(x)]
-#define AI_(x, y) Ai[(y) * TW + rp<SWZ, TW>(x)]
+#define A_(x, y) Ar[(y) * TW + rp<SW, TW>(x)]
+#define AI_(x, y) Ai[(y) * TW + rp<SW, TW>(x)]
   for (int j = 0; j < TW; ++j) {
     double d = A_(j, j);
     if (!(d > 0.0) || !isfinite(d)) return 1;
@@ -304,7 +307,7 @@ __device__ int warp_cholesky(double* Ar, double* Ai, int lane) {
 // with pivot=False, via _shorten_qr :487-500), bitwise in the reference's
 // sequential fma order.  Sequential chains over m make this slow; it only
 // runs for the rare pairs whose Grammian fails Cholesky.
-template <int TW, bool CPLX, bool SWZ>
+template <int TW, bool CPLX, int SW>
 __device__ int block_qr(const Plane& Y, int64_t c0, int64_t c1, int w, double* Sr, double* Si, double* outR,
                         double* outI, double* sh /* >= 3*TW + 8 doubles */) {
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -437,8 +440,8 @@ __device__ int block_qr(const Plane& Y, int64_t c0, int64_t c1, int w, double* S
   int bad = scal[3] != 0.0;
   for (int e = tid; e < TW * TW; e += nt) {
     int r = e % TW, c = e / TW;
-    outR[c * TW + rp<SWZ, TW>(r)] = S_(r, c);
-    if (CPLX) outI[c * TW + rp<SWZ, TW>(r)] = SI_(r, c);
+    outR[c * TW + rp<SW, TW>(r)] = S_(r, c);
+    if (CPLX) outI[c * TW + rp<SW, TW>(r)] = SI_(r, c);
   }
   __syncthreads();
   return bad;
@@ -488,7 +491,7 @@ struct InnerParams {
   int32_t* qr_locks;
 };
 
-template <int TW, bool CPLX, bool SWZ>
+template <int TW, bool CPLX, int SW>
 __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerParams P) {
   using Geo = InnerGeo<TW, CPLX>;
   constexpr int NPIV = Geo::NPIV;
@@ -524,11 +527,11 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
       for (int pl = 0; pl < NP; ++pl) {
         const double v = fold_splits(base + (int64_t)pl * TW * TW + e, (int64_t)NP * TW * TW, ns);
         if (pl == 0) {
-          M[0][c * TW + rp<SWZ, TW>(r)] = v;
-          M[0][r * TW + rp<SWZ, TW>(c)] = v;
+          M[0][c * TW + rp<SW, TW>(r)] = v;
+          M[0][r * TW + rp<SW, TW>(c)] = v;
         } else {
-          M[1][c * TW + rp<SWZ, TW>(r)] = r == c ? 0.0 : v;
-          M[1][r * TW + rp<SWZ, TW>(c)] = r == c ? 0.0 : -v;
+          M[1][c * TW + rp<SW, TW>(r)] = r == c ? 0.0 : v;
+          M[1][r * TW + rp<SW, TW>(c)] = r == c ? 0.0 : -v;
         }
       }
     }
@@ -539,12 +542,12 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   if (warp < 2 && !kc.shorten_qr) {
     double* Mr = warp == 0 ? S.A[0] : S.B[0];
     double* Mi = CPLX ? (warp == 0 ? S.A[NP - 1] : S.B[NP - 1]) : nullptr;
-    int f = warp_cholesky<TW, CPLX, SWZ>(Mr, Mi, lane);
+    int f = warp_cholesky<TW, CPLX, SW>(Mr, Mi, lane);
     if (lane == 0) S.chol_fail[warp] = f;
   }
   if (NW == 1 && !kc.shorten_qr) {  // a single warp: factor G after F
     __syncwarp();
-    int f = warp_cholesky<TW, CPLX, SWZ>(S.B[0], CPLX ? S.B[NP - 1] : nullptr, lane);
+    int f = warp_cholesky<TW, CPLX, SW>(S.B[0], CPLX ? S.B[NP - 1] : nullptr, lane);
     if (lane == 0) S.chol_fail[1] = f;
   }
   __syncthreads();
@@ -577,7 +580,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
     double* outR = mat == 0 ? S.A[0] : S.B[0];
     double* outI = CPLX ? (mat == 0 ? S.A[NP - 1] : S.B[NP - 1]) : nullptr;
     int w = TW / 2;
-    int bad = block_qr<TW, CPLX, SWZ>(Y, cp[0], cp[1], w, Sr, Si, outR, outI, qsh);
+    int bad = block_qr<TW, CPLX, SW>(Y, cp[0], cp[1], w, Sr, Si, outR, outI, qsh);
     __syncthreads();
     if (tid == 0) {
       __threadfence();
@@ -606,7 +609,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
       double z = 1.0;
       if (kc.prescale) {
         double br[EPL], bi[EPL], p[EPL];
-        load_col<TW, CPLX, SWZ>(Br, Bi, c, lane, br, bi);
+        load_col<TW, CPLX, SW>(Br, Bi, c, lane, br, bi);
         double ng2;
         if (kc.compensated) {  // _k_col_norm with comp (pointwise.py:260)
           double v = 0.0;
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
           z = 1.0 / sqrt(ng2);
           if (z != 1.0) {
             double ar[EPL], ai[EPL];
-            load_col<TW, CPLX, SWZ>(Ar, Ai, c, lane, ar, ai);
+            load_col<TW, CPLX, SW>(Ar, Ai, c, lane, ar, ai);
 #pragma unroll
             for (int e = 0; e < EPL; ++e) {
               ar[e] *= z;
@@ -631,12 +634,12 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
               br[e] *= z;
               bi[e] *= z;
             }
-            store_col<TW, CPLX, SWZ>(Ar, Ai, c, lane, ar, ai);
-            store_col<TW, CPLX, SWZ>(Br, Bi, c, lane, br, bi);
+            store_col<TW, CPLX, SW>(Ar, Ai, c, lane, ar, ai);
+            store_col<TW, CPLX, SW>(Br, Bi, c, lane, br, bi);
           }
         }
       }
-      if (lane == 0) Zr[c * TW + rp<SWZ, TW>(c)] = z;
+      if (lane == 0) Zr[c * TW + rp<SW, TW>(c)] = z;
     }
   }
   if (__syncthreads_or(pbad) && status == ST_OK) status = ST_RANK;
@@ -672,15 +675,15 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
         }
         double fi[RPL], fj[RPL], gi[RPL], gj[RPL];
         double fii[RPL], fji[RPL], gii[RPL], gji[RPL];
-        load_rows<TW, VEC, RPL, SWZ>(Ar, i, r0, fi);
-        load_rows<TW, VEC, RPL, SWZ>(Ar, j, r0, fj);
-        load_rows<TW, VEC, RPL, SWZ>(Br, i, r0, gi);
-        load_rows<TW, VEC, RPL, SWZ>(Br, j, r0, gj);
+        load_rows<TW, VEC, RPL, SW>(Ar, i, r0, fi);
+        load_rows<TW, VEC, RPL, SW>(Ar, j, r0, fj);
+        load_rows<TW, VEC, RPL, SW>(Br, i, r0, gi);
+        load_rows<TW, VEC, RPL, SW>(Br, j, r0, gj);
         if constexpr (CPLX) {
-          load_rows<TW, VEC, RPL, SWZ>(Ai, i, r0, fii);
-          load_rows<TW, VEC, RPL, SWZ>(Ai, j, r0, fji);
-          load_rows<TW, VEC, RPL, SWZ>(Bi, i, r0, gii);
-          load_rows<TW, VEC, RPL, SWZ>(Bi, j, r0, gji);
+          load_rows<TW, VEC, RPL, SW>(Ai, i, r0, fii);
+          load_rows<TW, VEC, RPL, SW>(Ai, j, r0, fji);
+          load_rows<TW, VEC, RPL, SW>(Bi, i, r0, gii);
+          load_rows<TW, VEC, RPL, SW>(Bi, j, r0, gji);
         } else {
 #pragma unroll
           for (int e = 0; e < RPL; ++e) fii[e] = fji[e] = gii[e] = gji[e] = 0.0;
@@ -793,11 +796,11 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
         bool swap = (flags & 4) != 0;
         double zi_[RPL], zj_[RPL], zii[RPL], zji[RPL];
         if (flags & 5) {
-          load_rows<TW, VEC, RPL, SWZ>(Zr, i, r0, zi_);
-          load_rows<TW, VEC, RPL, SWZ>(Zr, j, r0, zj_);
+          load_rows<TW, VEC, RPL, SW>(Zr, i, r0, zi_);
+          load_rows<TW, VEC, RPL, SW>(Zr, j, r0, zj_);
           if constexpr (CPLX) {
-            load_rows<TW, VEC, RPL, SWZ>(Zi, i, r0, zii);
-            load_rows<TW, VEC, RPL, SWZ>(Zi, j, r0, zji);
+            load_rows<TW, VEC, RPL, SW>(Zi, i, r0, zii);
+            load_rows<TW, VEC, RPL, SW>(Zi, j, r0, zji);
           }
           if (flags & 1) {
             const double z11 = z[0], z12r = z[1], z12i = z[2], z21r = z[3], z21i = z[4], z22 = z[5];
@@ -831,10 +834,10 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
           // (pointwise.py:211-214): park the updated F columns, let the
           // math lane read them whole
           if (flags & 1) {
-            store_rows<TW, VEC, RPL, SWZ>(Ar, i, r0, fi);
-            store_rows<TW, VEC, RPL, SWZ>(Ar, j, r0, fj);
-            store_rows<TW, VEC, RPL, SWZ>(Ai, i, r0, fii);
-            store_rows<TW, VEC, RPL, SWZ>(Ai, j, r0, fji);
+            store_rows<TW, VEC, RPL, SW>(Ar, i, r0, fi);
+            store_rows<TW, VEC, RPL, SW>(Ar, j, r0, fj);
+            store_rows<TW, VEC, RPL, SW>(Ai, i, r0, fii);
+            store_rows<TW, VEC, RPL, SW>(Ai, j, r0, fji);
           }
           __syncwarp();
           int sw_ = 0;
@@ -865,19 +868,19 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
         }
         if (flags & 5) {
           const int di = swap ? j : i, dj = swap ? i : j;
-          store_rows<TW, VEC, RPL, SWZ>(Ar, di, r0, fi);
-          store_rows<TW, VEC, RPL, SWZ>(Ar, dj, r0, fj);
-          store_rows<TW, VEC, RPL, SWZ>(Br, di, r0, gi);
-          store_rows<TW, VEC, RPL, SWZ>(Br, dj, r0, gj);
-          store_rows<TW, VEC, RPL, SWZ>(Zr, di, r0, zi_);
-          store_rows<TW, VEC, RPL, SWZ>(Zr, dj, r0, zj_);
+          store_rows<TW, VEC, RPL, SW>(Ar, di, r0, fi);
+          store_rows<TW, VEC, RPL, SW>(Ar, dj, r0, fj);
+          store_rows<TW, VEC, RPL, SW>(Br, di, r0, gi);
+          store_rows<TW, VEC, RPL, SW>(Br, dj, r0, gj);
+          store_rows<TW, VEC, RPL, SW>(Zr, di, r0, zi_);
+          store_rows<TW, VEC, RPL, SW>(Zr, dj, r0, zj_);
           if constexpr (CPLX) {
-            store_rows<TW, VEC, RPL, SWZ>(Ai, di, r0, fii);
-            store_rows<TW, VEC, RPL, SWZ>(Ai, dj, r0, fji);
-            store_rows<TW, VEC, RPL, SWZ>(Bi, di, r0, gii);
-            store_rows<TW, VEC, RPL, SWZ>(Bi, dj, r0, gji);
-            store_rows<TW, VEC, RPL, SWZ>(Zi, di, r0, zii);
-            store_rows<TW, VEC, RPL, SWZ>(Zi, dj, r0, zji);
+            store_rows<TW, VEC, RPL, SW>(Ai, di, r0, fii);
+            store_rows<TW, VEC, RPL, SW>(Ai, dj, r0, fji);
+            store_rows<TW, VEC, RPL, SW>(Bi, di, r0, gii);
+            store_rows<TW, VEC, RPL, SW>(Bi, dj, r0, gji);
+            store_rows<TW, VEC, RPL, SW>(Zi, di, r0, zii);
+            store_rows<TW, VEC, RPL, SW>(Zi, dj, r0, zji);
           }
         }
         // a rank-deficient pivot anywhere ends the solve (RankError upstream)
@@ -916,8 +919,8 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   if (status == ST_OK) {
     for (int c = warp; c < TW; c += NW) {
       double ar[EPL], ai[EPL], br[EPL], bi[EPL], p[EPL], q[EPL];
-      load_col<TW, CPLX, SWZ>(Ar, Ai, c, lane, ar, ai);
-      load_col<TW, CPLX, SWZ>(Br, Bi, c, lane, br, bi);
+      load_col<TW, CPLX, SW>(Ar, Ai, c, lane, ar, ai);
+      load_col<TW, CPLX, SW>(Br, Bi, c, lane, br, bi);
 #pragma unroll
       for (int e = 0; e < EPL; ++e) {
         p[e] = nrm_term<CPLX>(ar[e], ai[e]);
@@ -937,13 +940,13 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
         double th = 1.0 / sqrt(s);
         if (th != 1.0) {
           double zr[EPL], zi2[EPL];
-          load_col<TW, CPLX, SWZ>(Zr, Zi, c, lane, zr, zi2);
+          load_col<TW, CPLX, SW>(Zr, Zi, c, lane, zr, zi2);
 #pragma unroll
           for (int e = 0; e < EPL; ++e) {
             zr[e] *= th;
             zi2[e] *= th;
           }
-          store_col<TW, CPLX, SWZ>(Zr, Zi, c, lane, zr, zi2);
+          store_col<TW, CPLX, SW>(Zr, Zi, c, lane, zr, zi2);
         }
       }
     }
@@ -953,7 +956,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   // ---- exact-identity test (blocked.py:298-308) and outputs ---------------
   int nonid = 0;
   for (int e = tid; e < TW * TW; e += nt) {
-    double want = rp_inv<SWZ, TW>(e % TW) == (e / TW) ? 1.0 : 0.0;
+    double want = rp_inv<SW, TW>(e % TW) == (e / TW) ? 1.0 : 0.0;
     if (Zr[e] != want) nonid = 1;
     if (CPLX && Zi[e] != 0.0) nonid = 1;
   }
@@ -962,7 +965,7 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   double* zt = P.io.zt + (int64_t)pair * NP * TW * TW;
   for (int e = tid; e < NP * TW * TW; e += nt) {
     const int pl = e / (TW * TW), q = e % (TW * TW);
-    zt[pl * TW * TW + (q / TW) * TW + rp_inv<SWZ, TW>(q % TW)] = (&S.Z[0][0])[e];
+    zt[pl * TW * TW + (q / TW) * TW + rp_inv<SW, TW>(q % TW)] = (&S.Z[0][0])[e];
   }
   if (tid == 0) {
     P.io.ident[pair] = (nonid == 0 || status != ST_OK) ? 1 : 0;
@@ -975,12 +978,12 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
   }  // pairs
 }
 
-template <int TW, bool CPLX, bool SWZ>
+template <int TW, bool CPLX, int SW>
 int launch_inner_g(const InnerParams& p, cudaStream_t s) {
   const size_t smem = sizeof(InnerSmem<TW, CPLX>);
   static bool attr_done = false;
   if (!attr_done) {
-    cudaFuncSetAttribute(k_inner<TW, CPLX, SWZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_inner<TW, CPLX, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_done = true;
   }
   // HZG_INNER_CTAS caps the CTAs of one launch (each then serves several
@@ -1012,28 +1015,28 @@ int launch_inner_g(const InnerParams& p, cudaStream_t s) {
     at[0].val.priority = hi;
     lc.attrs = at;
     lc.numAttrs = 1;
-    cudaLaunchKernelEx(&lc, k_inner<TW, CPLX, SWZ>, p);
+    cudaLaunchKernelEx(&lc, k_inner<TW, CPLX, SW>, p);
   } else {
-    k_inner<TW, CPLX, SWZ><<<grid, InnerGeo<TW, CPLX>::NW * 32, smem, s>>>(p);
+    k_inner<TW, CPLX, SW><<<grid, InnerGeo<TW, CPLX>::NW * 32, smem, s>>>(p);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
 template <int TW, bool CPLX>
 int launch_inner_t(const InnerParams& p, cudaStream_t s) {
-  // swizzled rows for the 16-byte lane-group layout; the compensated
-  // variants read whole columns in natural order, so they keep it
-  if constexpr (TW == 8 || TW == 16 || TW == 32) {
-    if (!p.kc.compensated) return launch_inner_g<TW, CPLX, true>(p, s);
+  // swizzled rows (period = rows per lane) for the 16-byte lane-group
+  // layout; the compensated variants read whole columns in natural order
+  if constexpr (TW == 8 || TW == 16 || TW == 32 || (TW == 64 && !CPLX)) {
+    if (!p.kc.compensated) return launch_inner_g<TW, CPLX, InnerGeo<TW, CPLX>::RPL>(p, s);
   }
-  return launch_inner_g<TW, CPLX, false>(p, s);
+  return launch_inner_g<TW, CPLX, 0>(p, s);
 }
 
 // Single-block operations of the public API (cholesky_upper, qr_shorten,
 // blocked.py:345-363): the same device code the inner kernel uses.
 template <int TW, bool CPLX>
 __global__ void k_cholesky_op(double* Ar, double* Ai, int32_t* status) {
-  const int f = warp_cholesky<TW, CPLX, false>(Ar, Ai, threadIdx.x & 31);
+  const int f = warp_cholesky<TW, CPLX, 0>(Ar, Ai, threadIdx.x & 31);
   if (threadIdx.x == 0) *status = f;
 }
 
@@ -1041,7 +1044,7 @@ template <int TW, bool CPLX>
 __global__ void __launch_bounds__(256) k_qr_op(Plane Y, double* Sr, double* Si, double* outR, double* outI,
                                               int32_t* status) {
   __shared__ double qsh[3 * kMaxTW + 8];
-  const int bad = block_qr<TW, CPLX, false>(Y, 0, TW / 2, TW / 2, Sr, Si, outR, outI, qsh);
+  const int bad = block_qr<TW, CPLX, 0>(Y, 0, TW / 2, TW / 2, Sr, Si, outR, outI, qsh);
   if (threadIdx.x == 0) *status = bad;
 }
 

@@ -393,3 +393,18 @@ def test_sigma_vs_numpy_svd_of_F_Ginv(cplx):
     r = hz.solve(F, G, hz.SolverConfig(block_width=4))
     ref = np.linalg.svd(F @ np.linalg.inv(G), compute_uv=False)
     assert np.max(np.abs(np.sort(r.sigma)[::-1] - ref) / ref) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["genpair256_w16", "gauss200_w16", "corpus64_complex_w16"])
+def test_dmma_mode_w32_within_tolerance(name):
+    """2w = 64 (block_width 32): the warp-specialized DMMA Grammian and
+    postmultiply and the 8-rows-per-lane inner layout; sigma is independent
+    of the block width, so the reference's w=16 sigma is the yardstick."""
+    c = load_case(name)
+    r = hz.solve(c["F"], c["G"], _cfg(c, block_width=32))
+    nn = max(c["n"], 64)
+    assert r.converged
+    assert rel_err_sorted(r.sigma, c["sigma"]).max() <= 8 * nn * EPS
+    m = gsvd_metrics(c["F"], c["G"], r)
+    assert m["resF"] <= 4 * nn * EPS and m["resG"] <= 4 * nn * EPS
+    assert m["orthU"] <= 32 * nn * EPS and m["orthV"] <= 32 * nn * EPS

@@ -1,7 +1,6 @@
 out=gpurun_out
 tag=${1:-x}
-for pc in 1024 512 256; do for sr in 0 256; do
-  echo "post chunk $pc split rows $sr" >> $out/${tag}_explore.txt
-  if [ $sr = 0 ]; then HZG_POST_CHUNK=$pc timeout 900 python tools/explore.py 4096 cond 16 fb 100 >> $out/${tag}_explore.txt 2>&1;
-  else HZG_SPLIT_ROWS=$sr HZG_POST_CHUNK=$pc timeout 900 python tools/explore.py 4096 cond 16 fb 100 >> $out/${tag}_explore.txt 2>&1; fi
-done; done
+timeout 900 python tools/explore.py 16384 gauss 32 fb 2 >> $out/${tag}_explore.txt 2>&1
+timeout 900 python tools/explore.py 4096 gauss 32 fb 30 >> $out/${tag}_explore.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none -k regex:'k_' -c 40 --csv \
+    --log-file $out/${tag}_w32.csv python tools/prof_run.py 16384 12 gauss 32 > /dev/null 2>&1
