@@ -571,9 +571,10 @@ int hzg_init_fgz(hzg_ctx* c) {
 
 static int choose_groups(const hzg_ctx* c) {
   if (!c->wavefront) return 1;
-  // measured (profiles/r01_groups.txt): 8 groups at n = 4096, 4 at n = 16384
+  // measured without per-kernel events (bench.py, HZG_GROUPS sweep): 8
+  // groups at n = 4096 and n = 16384 (19.0 / 19.4 / 19.6 / 19.6 TFLOP/s for
+  // 2 / 4 / 6 / 8 groups at n = 16384)
   int g = std::max(1, std::min(8, c->npairs / 16));
-  if (c->npairs >= 256) g = 4;
   if (const char* e = std::getenv("HZG_GROUPS")) g = std::max(1, std::min(c->npairs, std::atoi(e)));
   return g;
 }
