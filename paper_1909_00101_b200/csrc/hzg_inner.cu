@@ -765,6 +765,9 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
           if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
             IeeeMath im;
             flags = pivot_scalar<CPLX>(im, kc, qv, z);
+#ifdef HZG_EXP_FALLBACK
+            if (P.io.phase) atomicAdd((unsigned long long*)&P.io.phase[0], 1000000000ull);
+#endif
           }
           if (flags & 1) {
             lane_applied += 1;

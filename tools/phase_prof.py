@@ -16,3 +16,4 @@ dev.run_steps(0, 20)
 torch.cuda.synchronize()
 dev.lib.hzg_debug_phases(dev.ctx, 0, out.ctypes.data_as(ctypes.c_void_p))
 print("steps", out[3], "cycles per inner step: A %.0f  B %.0f  C %.0f  total %.0f" % tuple(list(out[:3] / out[3]) + [out[:3].sum() / out[3]]))
+print("raw phase[0] (fallbacks x 1e9 when built with HZG_EXP_FALLBACK):", int(out[0]))
