@@ -459,8 +459,10 @@ __device__ __forceinline__ int pivot_scalar(M& m, const KernelCfg& kc, const dou
   if (!(a11 > 0.0 && a22 > 0.0 && b11 > 0.0 && b22 > 0.0)) return 8;
   double d11 = 1.0, d22 = 1.0;
   if (kc.per_step_rescale) rescale2(m, a11, a12r, a12i, a22, b11, b12r, b12i, b22, d11, d22);
-  if (gate<CPLX>(m, a11, a12r, a12i, a22, b12r, b12i, kc.epsn)) return (kc.sorting && a11 < a22) ? 4 : 0;
-  Xform X = transform<CPLX>(m, a11, a12r, a12i, a22, b12r, b12i);
+  double xb = -1.0;
+  if (gate<CPLX>(m, a11, a12r, a12i, a22, b12r, b12i, kc.epsn, &xb)) return (kc.sorting && a11 < a22) ? 4 : 0;
+  Xform X = CPLX ? transform_cplx(m, a11, a12r, a12i, a22, b12r, b12i, xb)
+                 : transform_real(m, a11, a12r, a22, b12r);
   const int bg = kc.crit_c2 ? !(X.cphi == 1.0 && X.cpsi == 1.0) : !(X.z11 == 1.0 && X.z22 == 1.0);
   int flags = 1 | (bg ? 2 : 0);
   if (kc.sorting && !CPLX) {
