@@ -83,6 +83,14 @@ int hzg_sweep(hzg_ctx* ctx, int64_t* total, int64_t* big);
  * bookkeeping (asynchronous; for profiling and bounded benchmarks). */
 int hzg_run_steps(hzg_ctx* ctx, int32_t first, int32_t count);
 
+/* Run pairs [p0, p0 + pn) of outer step `step` (Grammian, inner solve,
+ * postmultiply) on `stream` (NULL: the bound stream), asynchronously.  A
+ * rank of a multi-GPU job splits its slot range into contiguous groups on
+ * several streams so the streaming kernels of one group overlap the inner
+ * solves of another (the per-rank form of the wavefront sweep graph; the
+ * multi-worker step body of distsim.py:188-215, split by position). */
+int hzg_run_pairs(hzg_ctx* ctx, int32_t step, int32_t p0, int32_t pn, void* stream);
+
 /* Step-wise driving for multi-GPU jobs (one rank's slot range of the
  * ordering per GPU, blocks exchanged between steps by the caller):
  * hzg_collect folds the per-pair counters of all steps of the schedule

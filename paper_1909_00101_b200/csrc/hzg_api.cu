@@ -729,6 +729,14 @@ int hzg_run_steps(hzg_ctx* c, int32_t first, int32_t count) {
   return HZG_OK;
 }
 
+int hzg_run_pairs(hzg_ctx* c, int32_t step, int32_t p0, int32_t pn, void* stream) {
+  if (!c || !c->bound || step < 0 || step >= c->osteps || p0 < 0 || pn < 0 || p0 + pn > c->npairs)
+    return HZG_INVALID;
+  if (pn == 0) return HZG_OK;
+  int rc = launch_step(c, step, stream ? (cudaStream_t)stream : c->stream, nullptr, p0, pn);
+  return rc ? fail(c, rc, "step launch") : HZG_OK;
+}
+
 int hzg_collect(hzg_ctx* c, int64_t* total, int64_t* big) {
   if (!c || !c->bound) return HZG_INVALID;
   cudaError_t e;

@@ -95,6 +95,19 @@ class LocalTransport:
             for s, d in zip(_block_views(self.planes[src], b, self.w), _block_views(self.planes[dst], b, self.w)):
                 d.copy_(s)
 
+    def exchange_async(self, moves, waits, stream):
+        """exchange() on ``stream`` after the events ``waits`` (per rank, the
+        step's boundary groups); returns per-rank completion events."""
+        import torch
+        with torch.cuda.stream(stream):
+            for evs in waits:
+                for e in evs:
+                    stream.wait_event(e)
+            self.exchange(moves)
+            done = torch.cuda.Event()
+            done.record(stream)
+        return [done] * len(waits)
+
 
 class DistTransport:
     """torch.distributed point-to-point (NCCL between GPUs, gloo on CPU)."""
@@ -131,13 +144,28 @@ class DistTransport:
         for t, h in back:
             t.copy_(h)
 
+    def exchange_async(self, moves, waits, stream):
+        """exchange() ordered on ``stream``: the stream first waits for this
+        rank's boundary groups (``waits[0]``); NCCL's stream waits on it, and
+        wait() makes it wait for the transfers, so the returned event marks
+        the received blocks ready without a host synchronisation.  (gloo
+        stages through host memory; the device-to-host copies synchronise.)"""
+        import torch
+        with torch.cuda.stream(stream):
+            for e in waits[0]:
+                stream.wait_event(e)
+            self.exchange(moves)
+            done = torch.cuda.Event()
+            done.record(stream)
+        return [done]
+
 
 def gather_blocks(sched, k_final=0):
     """(block, owner, 0) moves bringing every block to rank 0 at step k_final."""
     return [(b, int(sched.owner[k_final, b]), 0) for b in range(sched.nblk) if sched.owner[k_final, b] != 0]
 
 
-def run_ranks(devs, sched, transport, cfg, allreduce=None, rescale_all=None):
+def run_ranks(devs, sched, transport, cfg, allreduce=None, wave=None):
     """The outer sweep loop (blocked.py:503-550) for block-partitioned ranks.
 
     devs: the DeviceGsvd objects this process drives (all R virtual ranks,
@@ -149,7 +177,7 @@ def run_ranks(devs, sched, transport, cfg, allreduce=None, rescale_all=None):
     sweeps = total = big = 0
     converged = False
     for _ in range(cfg.max_outer_sweeps):
-        t, b = sweep_ranks(devs, sched, transport, allreduce)
+        t, b = sweep_ranks(devs, sched, transport, allreduce, wave)
         sweeps += 1
         total += t
         big += b
@@ -159,15 +187,58 @@ def run_ranks(devs, sched, transport, cfg, allreduce=None, rescale_all=None):
     return sweeps, total, big, converged
 
 
-def sweep_ranks(devs, sched, transport, allreduce=None):
+def rank_groups(npairs, ngroups=None):
+    """Contiguous position groups [(p0, pn), ...] of one rank's slot range
+    for the per-rank wavefront (same rule as the single-GPU sweep graph,
+    hzg_api.cu choose_groups: 16+ pairs per group, at most 8 groups;
+    HZG_GROUPS overrides)."""
+    import os
+    if ngroups is None:
+        ngroups = max(1, min(8, npairs // 16))
+        if os.environ.get("HZG_GROUPS"):
+            ngroups = max(1, min(npairs, int(os.environ["HZG_GROUPS"])))
+    ngroups = max(1, min(npairs, ngroups))
+    return [(npairs * g // ngroups, npairs * (g + 1) // ngroups - npairs * g // ngroups) for g in range(ngroups)]
+
+
+class Wavefront:
+    """Streams and the group split of the per-rank wavefront.
+
+    Rank r's slot range is cut into G contiguous position groups, each on
+    its own stream.  Group g of step k+1 waits only for groups g-1, g, g+1
+    of step k on the same rank (a block moves by at most one position per
+    step); the two end groups also wait for the block exchange of step k,
+    which itself waits only for the end groups of step k (the blocks that
+    change owner sit at the ends of a range).  So the Grammian and
+    postmultiply streaming of some groups overlaps the latency-bound inner
+    solves of others, and the NCCL exchange overlaps the interior groups,
+    with no host synchronisation inside a sweep.  Per-pair work is the
+    same as the serialised schedule, so results stay bitwise equal."""
+
+    def __init__(self, devs, npairs, ngroups=None):
+        """npairs: slot-range length of every rank in ``devs``."""
+        import torch
+        self.torch = torch
+        self.groups = [rank_groups(np_, ngroups) for np_ in npairs]
+        self.streams = [[torch.cuda.Stream(device=d.device) for _ in gr] for d, gr in zip(devs, self.groups)]
+        self.comm = torch.cuda.Stream(device=devs[0].device)
+
+
+def sweep_ranks(devs, sched, transport, allreduce=None, wave=None):
     """One outer sweep of the partitioned schedule: every step on every
     rank with the block exchange after it, the counter sum, and the
     inter-sweep Z rescale when the sweep applied big transforms
-    (blocked.py:521-542).  Returns the sweep's (total, big)."""
-    for k in range(sched.steps):
-        for d in devs:
-            d.run_steps(k, 1)
-        transport.exchange(sched.moves(k))
+    (blocked.py:521-542).  Returns the sweep's (total, big).
+
+    wave: a Wavefront to run every rank's steps as position groups on
+    several streams (asynchronous exchange); None serialises step by step."""
+    if wave is None:
+        for k in range(sched.steps):
+            for d in devs:
+                d.run_steps(k, 1)
+            transport.exchange(sched.moves(k))
+    else:
+        _sweep_wavefront(devs, sched, transport, wave)
     t = b = 0
     for d in devs:
         tt, bb = d.collect()
@@ -181,6 +252,38 @@ def sweep_ranks(devs, sched, transport, allreduce=None):
     return t, b
 
 
+def _sweep_wavefront(devs, sched, transport, wave):
+    torch = wave.torch
+    main = torch.cuda.current_stream(devs[0].device)
+    start = torch.cuda.Event()
+    start.record(main)                   # after init / the previous rescale
+    prev = [[start] * len(gr) for gr in wave.groups]
+    xdone = [start] * len(devs)
+    for k in range(sched.steps):
+        cur = []
+        for r, d in enumerate(devs):
+            evs = []
+            G = len(wave.groups[r])
+            for g, (p0, pn) in enumerate(wave.groups[r]):
+                s = wave.streams[r][g]
+                for h in (g - 1, g, g + 1):
+                    if 0 <= h < G:
+                        s.wait_event(prev[r][h])
+                if g == 0 or g == G - 1:
+                    s.wait_event(xdone[r])
+                d.run_pairs(k, p0, pn, s)
+                e = torch.cuda.Event()
+                e.record(s)
+                evs.append(e)
+            cur.append(evs)
+        xdone = transport.exchange_async(sched.moves(k), [(evs[0], evs[-1]) for evs in cur], wave.comm)
+        prev = cur
+    for r in range(len(devs)):
+        for e in prev[r]:
+            main.wait_event(e)
+        main.wait_event(xdone[r])
+
+
 class PartitionedGsvd:
     """One rank of a block-partitioned solve over device-resident planes.
 
@@ -190,7 +293,7 @@ class PartitionedGsvd:
     _algorithm1_loop over the partitioned schedule; finalize() gathers the
     blocks to rank 0 and returns its device outputs (None elsewhere)."""
 
-    def __init__(self, planes, cfg, nranks, comm=None):
+    def __init__(self, planes, cfg, nranks, comm=None, wavefront=True):
         import torch
 
         from .solver import DeviceGsvd
@@ -228,12 +331,16 @@ class PartitionedGsvd:
                 return int(x[0]), int(x[1])
 
             self.allreduce = allreduce
+        ranks = range(self.nranks) if comm is None else [self.rank]
+        self.wave = None
+        if wavefront and torch.cuda.is_available():
+            self.wave = Wavefront(self.devs, [self.sched.ranges[r][1] - self.sched.ranges[r][0] for r in ranks])
         self.sweeps = self.total = self.big = 0
         self.converged = False
 
     def run(self):
         self.sweeps, self.total, self.big, self.converged = run_ranks(self.devs, self.sched, self.transport, self.cfg,
-                                                                      self.allreduce)
+                                                                      self.allreduce, self.wave)
         return self
 
     def init(self):
@@ -244,7 +351,7 @@ class PartitionedGsvd:
 
     def sweep(self):
         """One outer sweep (after init()); returns (total, big)."""
-        t, b = sweep_ranks(self.devs, self.sched, self.transport, self.allreduce)
+        t, b = sweep_ranks(self.devs, self.sched, self.transport, self.allreduce, self.wave)
         self.sweeps += 1
         self.total += t
         self.big += b
@@ -260,9 +367,11 @@ class PartitionedGsvd:
         return root.finalize(n0, mF0, mG0, sort=sort)
 
     def launch_counts(self):
-        # step-wise driving: 3 kernels per step, plus the counter fold and
-        # the Z rescale per sweep, per rank driven by this process
-        return len(self.devs) * (self.sched.steps * 3 + 2), len(self.devs) + 5
+        # step-wise driving: 3 kernels per step (per position group with the
+        # wavefront), plus the counter fold and the Z rescale per sweep, per
+        # rank driven by this process
+        g = sum(len(gr) for gr in self.wave.groups) if self.wave is not None else len(self.devs)
+        return self.sched.steps * 3 * g + 2 * len(self.devs), len(self.devs) + 5
 
     def close(self):
         for d in self.devs:
@@ -273,14 +382,15 @@ def epsn_of(cfg, n):
     return cfg.gate_eps * math.sqrt(n)
 
 
-def solve_blocks(F, G, cfg, nranks, comm=None):
+def solve_blocks(F, G, cfg, nranks, comm=None, wavefront=True):
     """GSVD of (F, G) with the block-partitioned schedule over nranks ranks.
 
     comm=None: nranks virtual ranks in this process on the current device
     (block exchange by device copies).  comm="dist": this process is one
     rank of an initialized torch.distributed job (NCCL, one GPU per rank);
     every rank passes the same F, G and rank 0 returns the result (the
-    others return None).  Results are bitwise those of nranks = 1.
+    others return None).  wavefront=False serialises each rank's steps
+    (no position groups).  Results are bitwise those of nranks = 1.
     """
     from .config import SolverConfig
     from .core import MatrixPlanePair, ProblemPair
@@ -296,7 +406,7 @@ def solve_blocks(F, G, cfg, nranks, comm=None):
     p = ProblemPair(F, G)
     w = cfg.block_width
     planes0, n, mF, mG = upload_bordered(p.F, p.G, w)
-    job = PartitionedGsvd(planes0, cfg, nranks, comm)
+    job = PartitionedGsvd(planes0, cfg, nranks, comm, wavefront=wavefront)
     try:
         job.run()
         out = job.finalize(p.n, p.F.rows, p.G.rows, sort=True)

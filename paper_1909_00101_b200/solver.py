@@ -161,6 +161,12 @@ class DeviceGsvd:
     def run_steps(self, first, count):
         _native.check(self.lib.hzg_run_steps(self.ctx, first, count), self.ctx, "run_steps")
 
+    def run_pairs(self, step, p0, pn, stream=None):
+        """Pairs [p0, p0 + pn) of outer step ``step`` on ``stream`` (a torch
+        stream; None: the bound stream), asynchronously."""
+        s = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+        _native.check(self.lib.hzg_run_pairs(self.ctx, step, p0, pn, s), self.ctx, "run_pairs")
+
     def finalize(self, n0=None, mF0=None, mG0=None, sort=True):
         """Final rescale, unborder, sort; returns device output tensors."""
         torch = self.torch

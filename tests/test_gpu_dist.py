@@ -22,8 +22,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, w, out):
+def _worker(rank, world, port, n, w, out, groups=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if groups:
+        os.environ["HZG_GROUPS"] = groups
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     import paper_1909_00101_b200 as hz
@@ -51,3 +53,12 @@ def test_solve_blocks_multiprocess_bitwise(world):
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), 256, 16, out), nprocs=world, join=True)
     assert out["ok"] and out["workers"] == world and out["rank1_none"]
+
+
+def test_solve_blocks_multiprocess_wavefront_groups():
+    """Two processes, 3 position groups per rank (8 pairs per rank at
+    n = 512): the event-ordered exchange against the single solve."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), 512, 16, out, "3"), nprocs=2, join=True)
+    assert out["ok"] and out["workers"] == 2 and out["rank1_none"]

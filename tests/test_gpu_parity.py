@@ -294,6 +294,30 @@ def test_block_partitioned_1024_eight_ranks():
     assert np.array_equal(r.sigma, one.sigma) and np.array_equal(r.Z.re, one.Z.re)
 
 
+@pytest.mark.parametrize("n,ranks,groups", [(2048, 2, None), (1024, 2, "3"), (1024, 4, "2"), (512, 3, "4")])
+def test_block_partitioned_wavefront_bitwise(n, ranks, groups, monkeypatch):
+    """Per-rank wavefront (position groups on several streams, block
+    exchange ordered by events, no host synchronisation inside a sweep)
+    against the step-serialised ranks and the single-GPU solve: bitwise.
+    n = 2048 / 2 ranks uses the default 4 groups of 16 pairs per rank."""
+    from paper_1909_00101_b200.dist import solve_blocks
+    g = O.gaussian_stream(n + ranks, 2 * n * n)
+    F = g[: n * n].reshape((n, n), order="F")
+    G = g[n * n:].reshape((n, n), order="F")
+    cfg = hz.SolverConfig(block_width=16)
+    one = hz.solve(F, G, cfg)
+    if groups:
+        monkeypatch.setenv("HZG_GROUPS", groups)
+    wave = solve_blocks(F, G, cfg, ranks)
+    serial = solve_blocks(F, G, cfg, ranks, wavefront=False)
+    for r in (wave, serial):
+        assert r.workers == ranks
+        assert (r.sweeps, r.total_transforms, r.big_transforms) == (one.sweeps, one.total_transforms,
+                                                                    one.big_transforms)
+        for a, b in ((r.sigma, one.sigma), (r.U.re, one.U.re), (r.V.re, one.V.re), (r.Z.re, one.Z.re)):
+            assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("name", ["genpair256_w16", "gauss200_w16", "corpus64_real_w16", "gauss1024"])
 def test_fused_postgram_bitwise_equals_unfused(name, monkeypatch):
     """The fused postmultiply(k) + Grammian(k+1) kernel (k_postgram) must give

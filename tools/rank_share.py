@@ -1,0 +1,85 @@
+"""Per-rank sweep time of the block-partitioned schedule, measured on one GPU.
+
+One rank r of an R-rank job runs its slot range of every step (Grammian,
+inner, postmultiply of its pairs) on the GPU alone; the block exchange is
+replaced by event bookkeeping only (blocks are not copied: the columns that
+would arrive keep stale, valid values, so the per-step work has the same
+shape).  The slowest rank's sweep time bounds the R-GPU sweep from below
+(NCCL moves at most 2 blocks per rank and step, overlapped with the
+interior groups), so F_sweep / max_r(t_r) estimates strong scaling on R
+B200s where only one GPU is available.
+
+usage: python tools/rank_share.py N R[,R...] [wave|serial] [sweeps]
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bench
+import paper_1909_00101_b200 as hz
+from paper_1909_00101_b200 import dist as D
+
+
+class NullTransport:
+    def exchange(self, moves):
+        pass
+
+    def exchange_async(self, moves, waits, stream):
+        with torch.cuda.stream(stream):
+            for e in waits[0]:
+                stream.wait_event(e)
+            done = torch.cuda.Event()
+            done.record(stream)
+        return [done]
+
+
+def main():
+    n = int(sys.argv[1])
+    Rs = [int(x) for x in sys.argv[2].split(",")]
+    mode = sys.argv[3] if len(sys.argv) > 3 else "wave"
+    nsw = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+    w = 16
+
+    class A:
+        pass
+    a = A()
+    a.n, a.kind, a.seed, a.w = n, "gauss", 7, w
+    F0, G0, _ = bench.gen_pair(a, torch, torch.device("cuda"))
+    Fsw = bench.flops_per_sweep(n, n, n, w)
+    cfg = hz.SolverConfig(block_width=w, max_outer_sweeps=100)
+    for R in Rs:
+        sched = D.BlockSchedule(n // w, R)
+        worst = 0.0
+        for r in sorted({0, R // 2, R - 1}):
+            Fw, Gw = F0.clone(), G0.clone()
+            dev = hz.DeviceGsvd({"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}, cfg, epsn=D.epsn_of(cfg, n),
+                                schedule=sched.colpairs(r, w))
+            lo, hi = sched.ranges[r]
+            wave = D.Wavefront([dev], [hi - lo]) if mode == "wave" else None
+            dev.init()
+            D.sweep_ranks([dev], sched, NullTransport(), None, wave)   # warm-up sweep
+            times = []
+            for _ in range(nsw):
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                D.sweep_ranks([dev], sched, NullTransport(), None, wave)
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1) / 1e3)
+            t = sorted(times)[len(times) // 2]
+            worst = max(worst, t)
+            g = len(wave.groups[0]) if wave else 1
+            print(f"n={n} R={R} rank {r}: {hi - lo} pairs/step, {g} groups, {mode}: sweep {t * 1e3:.1f} ms",
+                  flush=True)
+            dev.close()
+            del dev, Fw, Gw
+        print(f"n={n} R={R} {mode}: slowest rank {worst * 1e3:.1f} ms/sweep -> "
+              f"{Fsw / worst / 1e12:.2f} TF/s job, {Fsw / worst / 1e12 / R:.2f} TF/s per GPU", flush=True)
+
+
+if __name__ == "__main__":
+    main()
