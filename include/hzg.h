@@ -91,6 +91,23 @@ int hzg_run_steps(hzg_ctx* ctx, int32_t first, int32_t count);
  * multi-worker step body of distsim.py:188-215, split by position). */
 int hzg_run_pairs(hzg_ctx* ctx, int32_t step, int32_t p0, int32_t pn, void* stream);
 
+/* The same per-rank wavefront driven from the library, one call per step
+ * (no per-group host work): hzg_wave_step runs step `step` as `groups`
+ * contiguous position groups on library-owned streams.  Group g waits for
+ * groups g-1, g, g+1 of the previous step; the two end groups also wait
+ * for everything queued on `comm` (the caller's block exchange of the
+ * previous step), and `comm` is made to wait for this step's end groups,
+ * so the caller queues the next exchange on `comm` right after the call.
+ * In DMMA mode the Z postmultiply runs on separate low-priority streams;
+ * with `zcomm` non-NULL the Z blocks are exchanged on `zcomm` instead of
+ * `comm` (the caller queues them there), so the Z updates stay off the
+ * step chain.  Step 0 (or a break in the sequence) starts after the work
+ * queued on the bound stream.  hzg_wave_join makes the bound stream wait
+ * for the last step, `comm` and `zcomm` (before hzg_collect /
+ * hzg_finalize). */
+int hzg_wave_step(hzg_ctx* ctx, int32_t step, int32_t groups, void* comm, void* zcomm);
+int hzg_wave_join(hzg_ctx* ctx, void* comm, void* zcomm);
+
 /* Step-wise driving for multi-GPU jobs (one rank's slot range of the
  * ordering per GPU, blocks exchanged between steps by the caller):
  * hzg_collect folds the per-pair counters of all steps of the schedule

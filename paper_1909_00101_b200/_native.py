@@ -24,7 +24,7 @@ class HzgConfig(ctypes.Structure):
 
 
 EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_init_fgz", "hzg_sweep",
-           "hzg_run_steps", "hzg_run_pairs", "hzg_collect", "hzg_rescale_z", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
+           "hzg_run_steps", "hzg_run_pairs", "hzg_wave_step", "hzg_wave_join", "hzg_collect", "hzg_rescale_z", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
            "hzg_step_counters", "hzg_debug_phases", "hzg_launch_counts", "hzg_op_grammian",
            "hzg_op_cholesky_upper", "hzg_op_qr_shorten", "hzg_op_postmultiply", "hzg_op_rescale", "hzg_test_fastmath", "hzg_last_error",
            "hzg_destroy")
@@ -60,6 +60,10 @@ def load(path=LIB_PATH):
         L.hzg_run_steps.restype = ctypes.c_int
         L.hzg_run_pairs.argtypes = [P, I32, I32, I32, P]
         L.hzg_run_pairs.restype = ctypes.c_int
+        L.hzg_wave_step.argtypes = [P, I32, I32, P, P]
+        L.hzg_wave_step.restype = ctypes.c_int
+        L.hzg_wave_join.argtypes = [P, P, P]
+        L.hzg_wave_join.restype = ctypes.c_int
         L.hzg_collect.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.hzg_collect.restype = ctypes.c_int
         L.hzg_rescale_z.argtypes = [P]

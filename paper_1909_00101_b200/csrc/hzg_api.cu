@@ -44,8 +44,17 @@ struct hzg_ctx {
   int32_t* d_pg_links = nullptr;
   int32_t* d_pg_exc = nullptr;
   int32_t* d_all_pairs = nullptr;
-  std::vector<cudaStream_t> gstreams;
-  std::vector<cudaEvent_t> gevents;  // fork, joins[G], step events [2][G]
+  std::vector<cudaStream_t> gstreams;  // [G] step chains (high priority)
+  std::vector<cudaStream_t> zstreams;  // [G] deferred-Z chains (low priority)
+  std::vector<cudaEvent_t> gevents;    // fork, joins[G], step events [2][G], inner done [G], Z events [2][G], Z joins [G]
+  // step-wise wavefront of one rank (hzg_wave_step): streams, events
+  // [start, exchange tail, step events [2][G]], groups, last step run
+  std::vector<cudaStream_t> wstreams, wzstreams;
+  std::vector<cudaEvent_t> wevents;
+  int wgroups = 0;
+  int wlast = -1;
+  int wfirst = 0;
+  bool wdz = false;
   std::vector<int32_t> colpair_host;  // [osteps][npairs][2]
   std::vector<int32_t> itable_host;   // [isteps][tw]
   // device state
@@ -59,6 +68,9 @@ struct hzg_ctx {
   int32_t* d_itable = nullptr;
   GramWS gw{};
   InnerOut io{};
+  double* zt2 = nullptr;       // odd-step transforms (see io_of)
+  int32_t* ident2 = nullptr;
+  bool defer_z = false;        // Z postmultiply on its own streams, off the step chain
   int64_t* d_ctr = nullptr;    // 4 int64: total, big, status, pad
   int32_t* d_status = nullptr; // init/final status
   double* d_qr = nullptr;
@@ -202,7 +214,7 @@ void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
 }
 
 struct Layout {
-  size_t colpair, itable, part, zt, ident, counts, ctr, status, qr, qrlock, fin, sig, phase, comp, pg, total;
+  size_t colpair, itable, part, zt, ident, zt2, ident2, counts, ctr, status, qr, qrlock, fin, sig, phase, comp, pg, total;
 };
 
 Layout layout(const hzg_ctx* c) {
@@ -219,6 +231,10 @@ Layout layout(const hzg_ctx* c) {
   L.part = take((size_t)c->npairs * 2 * c->gw.smax * NP * c->tw * c->tw * 8);
   L.zt = take((size_t)c->npairs * NP * c->tw * c->tw * 8);
   L.ident = take((size_t)c->npairs * 4);
+  // second transform buffer (odd steps): the deferred Z postmultiply of
+  // step k still reads its transforms while step k+1's inner solve writes
+  L.zt2 = take((size_t)c->npairs * NP * c->tw * c->tw * 8);
+  L.ident2 = take((size_t)c->npairs * 4);
   L.counts = take((size_t)c->osteps * c->npairs * 4 * 4);
   L.ctr = take(4 * 8);
   L.status = take(4 * 4);
@@ -268,9 +284,26 @@ void record(cudaEvent_t e, cudaStream_t s) {
     cudaEventRecord(e, s);
 }
 
-int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr, int p0 = 0, int pn = -1) {
+// transforms of step `step`: even and odd steps alternate between two
+// buffers, so a deferred Z postmultiply of step k can run beside step k+1
+InnerOut io_of(const hzg_ctx* c, int step) {
+  InnerOut o = c->io;
+  if (step & 1) {
+    o.zt = c->zt2;
+    o.ident = c->ident2;
+  }
+  return o;
+}
+
+// One outer step on pairs [p0, p0 + pn): Grammian, inner solve,
+// postmultiply.  defer_z: postmultiply F and G only (the caller runs
+// launch_step_z for Z on another stream); inner_done: recorded after the
+// inner solve.
+int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr, int p0 = 0, int pn = -1,
+                bool defer_z = false, cudaEvent_t inner_done = nullptr) {
   StepPairs sp{c->d_colpair, c->npairs, p0, pn < 0 ? c->npairs : pn};
   KernelCfg kc = kernel_cfg(c);
+  const InnerOut io = io_of(c, step);
   if (ev) record(ev[0], s);
   int rc = HZG_OK;
   if (c->cfg.shorten_qr) {
@@ -283,15 +316,25 @@ int launch_step(hzg_ctx* c, int step, cudaStream_t s, cudaEvent_t* ev = nullptr,
   }
   if (rc) return rc;
   if (ev) record(ev[1], s);
-  rc = launch_inner(c->F, c->G, sp, step, kc, c->gw, c->d_itable, c->isteps, c->io, c->d_qr, c->qr_slots,
+  rc = launch_inner(c->F, c->G, sp, step, kc, c->gw, c->d_itable, c->isteps, io, c->d_qr, c->qr_slots,
                     c->d_qrlock, s);
   if (rc) return rc;
+  if (inner_done) cudaEventRecord(inner_done, s);
   if (ev) record(ev[2], s);
-  rc = c->use_dmma ? launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s)
-                   : launch_postmult_exact(c->F, c->G, c->Z, sp, step, c->w, c->cplx, c->io, s);
+  if (defer_z)
+    rc = launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, io, s, 0, 2);
+  else
+    rc = c->use_dmma ? launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, io, s)
+                     : launch_postmult_exact(c->F, c->G, c->Z, sp, step, c->w, c->cplx, io, s);
   if (rc) return rc;
   if (ev) record(ev[3], s);
   return HZG_OK;
+}
+
+// the deferred Z postmultiply of step `step` on pairs [p0, p0 + pn)
+int launch_step_z(hzg_ctx* c, int step, cudaStream_t s, int p0, int pn) {
+  StepPairs sp{c->d_colpair, c->npairs, p0, pn};
+  return launch_postmult_dmma(c->F, c->G, c->Z, sp, step, c->w, c->cplx, io_of(c, step), s, 2, 1);
 }
 
 void accumulate_times(hzg_ctx* c) {
@@ -496,6 +539,8 @@ int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double*
   c->gw.part = (double*)(c->ws + L.part);
   c->io.zt = (double*)(c->ws + L.zt);
   c->io.ident = (int32_t*)(c->ws + L.ident);
+  c->zt2 = (double*)(c->ws + L.zt2);
+  c->ident2 = (int32_t*)(c->ws + L.ident2);
   c->io.counts = (int32_t*)(c->ws + L.counts);
   c->d_ctr = (int64_t*)(c->ws + L.ctr);
   c->d_status = (int32_t*)(c->ws + L.status);
@@ -584,18 +629,41 @@ static int choose_groups(const hzg_ctx* c) {
 // stream; group g of step k+1 waits only for groups g-1, g, g+1 of step k
 // (the pairs its blocks come from), so Grammian / postmultiply streaming of
 // some groups overlaps the latency-bound inner solves of others.
+// grow a pool of non-blocking streams to n; chain streams get the highest
+// scheduling priority and deferred-Z streams the lowest (HZG_PRIO=0: all
+// default), so the Z postmultiply fills the SMs and bandwidth the step chain
+// leaves idle (mostly during the latency-bound inner solves)
+static int stream_pool(hzg_ctx* c, std::vector<cudaStream_t>& pool, int n, bool high) {
+  static int use = -1;
+  if (use < 0) {
+    const char* e = std::getenv("HZG_PRIO");
+    use = e ? std::atoi(e) : 1;
+  }
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  while ((int)pool.size() < n) {
+    cudaStream_t st;
+    cudaError_t e = cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, use ? (high ? greatest : least) : 0);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamCreate");
+    pool.push_back(st);
+  }
+  return HZG_OK;
+}
+
+static bool want_defer_z(const hzg_ctx* c) {
+  // the Z postmultiply leaves the step chain (F, G feed the next step's
+  // Grammians, Z only its own later updates): DMMA mode, unfused, untimed
+  const char* e = std::getenv("HZG_DEFER_Z");
+  return c->use_dmma && !c->fused && !c->timing && !(e && std::atoi(e) == 0);
+}
+
 static int build_graph(hzg_ctx* c) {
   cudaError_t e;
   const int G = c->groups = choose_groups(c);
-  if ((int)c->gstreams.size() < G) {
-    for (int g = (int)c->gstreams.size(); g < G; ++g) {
-      cudaStream_t st;
-      if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess)
-        return cuda_fail(c, e, "cudaStreamCreate");
-      c->gstreams.push_back(st);
-    }
-  }
-  const size_t nev = 1 + (size_t)G + 2 * (size_t)G;
+  const bool dz = c->defer_z = want_defer_z(c);
+  if (int rc = stream_pool(c, c->gstreams, G, true)) return rc;
+  if (int rc = stream_pool(c, c->zstreams, dz ? G : 0, false)) return rc;
+  const size_t nev = 1 + (size_t)G + 2 * (size_t)G + 4 * (size_t)G;
   while (c->gevents.size() < nev) {
     cudaEvent_t ev;
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
@@ -605,6 +673,9 @@ static int build_graph(hzg_ctx* c) {
   cudaEvent_t fork = c->gevents[0];
   cudaEvent_t* join = &c->gevents[1];
   cudaEvent_t* stepev = &c->gevents[1 + G];  // [2][G]
+  cudaEvent_t* idone = &c->gevents[1 + 3 * G];  // [G]
+  cudaEvent_t* zev = &c->gevents[1 + 4 * G];    // [2][G]
+  cudaEvent_t* zjoin = &c->gevents[1 + 6 * G];  // [G]
   if (c->timing && c->tev.empty()) {
     c->tev.resize((size_t)c->osteps * G * 4);
     for (auto& ev : c->tev) cudaEventCreate(&ev);
@@ -647,14 +718,33 @@ static int build_graph(hzg_ctx* c) {
         if (g > 0) cudaStreamWaitEvent(s, stepev[((st - 1) & 1) * G + g - 1], 0);
         if (g + 1 < G) cudaStreamWaitEvent(s, stepev[((st - 1) & 1) * G + g + 1], 0);
       }
+      // the inner solve of step st overwrites the transforms the deferred
+      // Z postmultiply of step st - 2 (same pairs) reads
+      if (dz && st >= 2) cudaStreamWaitEvent(s, zev[(st & 1) * G + g], 0);
       const int p0 = (int)((int64_t)c->npairs * g / G), p1 = (int)((int64_t)c->npairs * (g + 1) / G);
-      rc = launch_step(c, st, s, c->timing ? &c->tev[((size_t)st * G + g) * 4] : nullptr, p0, p1 - p0);
+      rc = launch_step(c, st, s, c->timing ? &c->tev[((size_t)st * G + g) * 4] : nullptr, p0, p1 - p0, dz,
+                       dz ? idone[g] : nullptr);
       cudaEventRecord(stepev[(st & 1) * G + g], s);
+      if (dz && rc == HZG_OK) {
+        // Z chain of the group: its transforms, and the Z blocks of groups
+        // g-1 .. g+1 from the previous step
+        cudaStream_t z = c->zstreams[g];
+        cudaStreamWaitEvent(z, idone[g], 0);
+        if (st > 0)
+          for (int h = g - 1; h <= g + 1; ++h)
+            if (h >= 0 && h < G) cudaStreamWaitEvent(z, zev[((st - 1) & 1) * G + h], 0);
+        rc = launch_step_z(c, st, z, p0, p1 - p0);
+        cudaEventRecord(zev[(st & 1) * G + g], z);
+      }
     }
   }
   for (int g = 0; g < G; ++g) {
     cudaEventRecord(join[g], c->gstreams[g]);
     cudaStreamWaitEvent(c->cap, join[g], 0);
+    if (dz) {
+      cudaEventRecord(zjoin[g], c->zstreams[g]);
+      cudaStreamWaitEvent(c->cap, zjoin[g], 0);
+    }
   }
   if (rc == HZG_OK) rc = launch_counters(c->io.counts, (int64_t)c->osteps * c->npairs, c->d_ctr, c->cap);
   if (rc == HZG_OK)
@@ -668,7 +758,9 @@ static int build_graph(hzg_ctx* c) {
   }
   if (e != cudaSuccess) return cuda_fail(c, e, "end capture");
   c->graph = g;
-  if ((e = cudaGraphInstantiate(&c->gexec, g, 0)) != cudaSuccess) return cuda_fail(c, e, "graph instantiate");
+  // honour the captured per-node priorities (chain vs deferred Z)
+  if ((e = cudaGraphInstantiate(&c->gexec, g, cudaGraphInstantiateFlagUseNodePriority)) != cudaSuccess)
+    return cuda_fail(c, e, "graph instantiate");
   return HZG_OK;
 }
 
@@ -735,6 +827,103 @@ int hzg_run_pairs(hzg_ctx* c, int32_t step, int32_t p0, int32_t pn, void* stream
   if (pn == 0) return HZG_OK;
   int rc = launch_step(c, step, stream ? (cudaStream_t)stream : c->stream, nullptr, p0, pn);
   return rc ? fail(c, rc, "step launch") : HZG_OK;
+}
+
+int hzg_wave_step(hzg_ctx* c, int32_t step, int32_t groups, void* comm, void* zcomm) {
+  if (!c || !c->bound || step < 0 || step >= c->osteps || groups < 1) return HZG_INVALID;
+  cudaError_t e;
+  const int G = std::min<int>(groups, c->npairs);
+  if (int rc = stream_pool(c, c->wstreams, G, true)) return rc;
+  if (int rc = stream_pool(c, c->wzstreams, G, false)) return rc;
+  while (c->wevents.size() < 3 + 5 * (size_t)G) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(c, e, "cudaEventCreate");
+    c->wevents.push_back(ev);
+  }
+  cudaStream_t cs = comm ? (cudaStream_t)comm : c->stream;
+  cudaEvent_t start = c->wevents[0], xtail = c->wevents[1];
+  cudaEvent_t* sev = &c->wevents[2];           // [2][G] step chains
+  cudaEvent_t* idone = &c->wevents[2 + 2 * G];  // [G] inner solves done
+  cudaEvent_t* zev = &c->wevents[2 + 3 * G];    // [2][G] deferred-Z chains
+  cudaEvent_t ztail = c->wevents[2 + 5 * G];
+  // deferred Z in the step-wise wavefront: opt-in (HZG_WAVE_DEFER_Z=1); on
+  // one rank's share (tools/rank_share.py) it measured slower at 2-4 ranks
+  // of n = 16384 and even at 8
+  const char* wdz_env = std::getenv("HZG_WAVE_DEFER_Z");
+  const bool dz = want_defer_z(c) && wdz_env && std::atoi(wdz_env) != 0;
+  // zcomm: the Z blocks travel in their own exchange (off the step chain
+  // when the Z postmultiply is deferred)
+  cudaStream_t zs = zcomm ? (cudaStream_t)zcomm : nullptr;
+  // a new chain (first step of a sweep, or a different group count or
+  // deferral) starts after everything already queued on the bound stream
+  const bool fresh = step == 0 || c->wgroups != G || c->wlast != step - 1 || c->wdz != dz;
+  if (fresh) {
+    cudaEventRecord(start, c->stream);
+    c->wfirst = step;
+  }
+  // the block exchange of the previous step, queued on the comm stream
+  cudaEventRecord(xtail, cs);
+  if (zs) cudaEventRecord(ztail, zs);
+  for (int g = 0; g < G; ++g) {
+    cudaStream_t s = c->wstreams[g];
+    if (fresh) {
+      cudaStreamWaitEvent(s, start, 0);
+    } else {
+      for (int h = g - 1; h <= g + 1; ++h)
+        if (h >= 0 && h < G) cudaStreamWaitEvent(s, sev[((step - 1) & 1) * G + h], 0);
+    }
+    if (g == 0 || g == G - 1) {
+      cudaStreamWaitEvent(s, xtail, 0);
+      if (zs && !dz) cudaStreamWaitEvent(s, ztail, 0);  // this chain's postmultiply writes Z
+    }
+    // transforms of step - 2 (same buffer) read by its deferred Z postmultiply
+    if (dz && step - 2 >= c->wfirst) cudaStreamWaitEvent(s, zev[(step & 1) * G + g], 0);
+    const int p0 = (int)((int64_t)c->npairs * g / G), p1 = (int)((int64_t)c->npairs * (g + 1) / G);
+    int rc = launch_step(c, step, s, nullptr, p0, p1 - p0, dz, dz ? idone[g] : nullptr);
+    if (rc) return fail(c, rc, "step launch");
+    cudaEventRecord(sev[(step & 1) * G + g], s);
+    if (dz) {
+      cudaStream_t z = c->wzstreams[g];
+      cudaStreamWaitEvent(z, idone[g], 0);
+      if (zs && (g == 0 || g == G - 1)) cudaStreamWaitEvent(z, ztail, 0);
+      if (step - 1 >= c->wfirst)
+        for (int h = g - 1; h <= g + 1; ++h)
+          if (h >= 0 && h < G) cudaStreamWaitEvent(z, zev[((step - 1) & 1) * G + h], 0);
+      if ((rc = launch_step_z(c, step, z, p0, p1 - p0))) return fail(c, rc, "step launch");
+      cudaEventRecord(zev[(step & 1) * G + g], z);
+    }
+  }
+  // the next exchange (queued on comm by the caller) reads the end groups'
+  // blocks of F, G and Z
+  for (int g : {0, G - 1}) {
+    cudaStreamWaitEvent(cs, sev[(step & 1) * G + g], 0);
+    if (dz) cudaStreamWaitEvent(zs ? zs : cs, zev[(step & 1) * G + g], 0);
+    else if (zs) cudaStreamWaitEvent(zs, sev[(step & 1) * G + g], 0);
+  }
+  c->wgroups = G;
+  c->wlast = step;
+  c->wdz = dz;
+  return HZG_OK;
+}
+
+int hzg_wave_join(hzg_ctx* c, void* comm, void* zcomm) {
+  if (!c || !c->bound) return HZG_INVALID;
+  if (c->wlast < 0) return HZG_OK;
+  const int G = c->wgroups;
+  cudaStream_t cs = comm ? (cudaStream_t)comm : c->stream;
+  for (int g = 0; g < G; ++g) {
+    cudaStreamWaitEvent(c->stream, c->wevents[2 + (c->wlast & 1) * G + g], 0);
+    if (c->wdz) cudaStreamWaitEvent(c->stream, c->wevents[2 + 3 * G + (c->wlast & 1) * G + g], 0);
+  }
+  cudaEventRecord(c->wevents[1], cs);
+  cudaStreamWaitEvent(c->stream, c->wevents[1], 0);
+  if (zcomm) {
+    cudaEventRecord(c->wevents[2 + 5 * G], (cudaStream_t)zcomm);
+    cudaStreamWaitEvent(c->stream, c->wevents[2 + 5 * G], 0);
+  }
+  c->wlast = -1;
+  return HZG_OK;
 }
 
 int hzg_collect(hzg_ctx* c, int64_t* total, int64_t* big) {
@@ -899,8 +1088,10 @@ int hzg_debug_phases(hzg_ctx* c, int32_t enable, int64_t* out4) {
 int hzg_launch_counts(const hzg_ctx* c, int64_t* per_sweep, int64_t* per_solve_fixed) {
   if (!c) return HZG_INVALID;
   const int G = c->gexec ? c->groups : choose_groups(c);
-  // sweep graph: 3 step kernels per (step, group), counter fold, rescale
-  if (per_sweep) *per_sweep = (int64_t)c->osteps * G * 3 + 2;
+  // sweep graph: 3 step kernels per (step, group) (4 with the deferred Z
+  // postmultiply), counter fold, rescale
+  const bool dz = c->gexec ? c->defer_z : want_defer_z(c);
+  if (per_sweep) *per_sweep = (int64_t)c->osteps * G * (dz ? 4 : 3) + 2;
   if (per_sweep && c->fused) {
     int64_t n = 1 + 2 + (int64_t)c->osteps * 1 + (int64_t)(c->osteps - 1) * 2 + 1;  // gram0, counters, rescale, inner, postgram+postZ, last post
     for (int k = 0; k + 1 < c->osteps; ++k) n += c->pg_nexc[k] > 0 ? 1 : 0;
@@ -1044,6 +1235,10 @@ void hzg_destroy(hzg_ctx* c) {
   for (auto& e : c->rev) cudaEventDestroy(e);
   for (auto& e : c->gevents) cudaEventDestroy(e);
   for (auto& s : c->gstreams) cudaStreamDestroy(s);
+  for (auto& e : c->wevents) cudaEventDestroy(e);
+  for (auto& s : c->wstreams) cudaStreamDestroy(s);
+  for (auto& s : c->zstreams) cudaStreamDestroy(s);
+  for (auto& s : c->wzstreams) cudaStreamDestroy(s);
   delete c;
 }
 

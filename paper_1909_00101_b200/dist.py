@@ -25,6 +25,7 @@ Transports:
 """
 
 import math
+import os
 
 import numpy as np
 
@@ -71,16 +72,21 @@ class BlockSchedule:
         return np.nonzero(self.owner[k] == rank)[0]
 
 
-def _block_views(planes, b, w):
+def _block_views(planes, b, w, keys=("Fr", "Fi", "Gr", "Gi", "Zr", "Zi")):
     """Contiguous (w, m) views of block b of every plane (column-major planes
     are stored as (cols, rows) tensors, so w consecutive columns are one
     contiguous chunk)."""
     out = []
-    for key in ("Fr", "Fi", "Gr", "Gi", "Zr", "Zi"):
+    for key in keys:
         t = planes.get(key)
         if t is not None:
             out.append(t[b * w:(b + 1) * w])
     return out
+
+
+_ALL = ("Fr", "Fi", "Gr", "Gi", "Zr", "Zi")
+_FG = ("Fr", "Fi", "Gr", "Gi")
+_Z = ("Zr", "Zi")
 
 
 class LocalTransport:
@@ -90,74 +96,76 @@ class LocalTransport:
         self.planes = planes_by_rank
         self.w = w
 
-    def exchange(self, moves):
+    def exchange(self, moves, keys=_ALL):
         for (b, src, dst) in moves:
-            for s, d in zip(_block_views(self.planes[src], b, self.w), _block_views(self.planes[dst], b, self.w)):
+            for s, d in zip(_block_views(self.planes[src], b, self.w, keys),
+                            _block_views(self.planes[dst], b, self.w, keys)):
                 d.copy_(s)
 
-    def exchange_async(self, moves, waits, stream):
-        """exchange() on ``stream`` after the events ``waits`` (per rank, the
-        step's boundary groups); returns per-rank completion events."""
+    def exchange_on(self, moves, stream, zstream=None):
+        """exchange() queued on ``stream`` (the wavefront's exchange stream);
+        with ``zstream`` the Z blocks go on that stream instead."""
         import torch
         with torch.cuda.stream(stream):
-            for evs in waits:
-                for e in evs:
-                    stream.wait_event(e)
-            self.exchange(moves)
-            done = torch.cuda.Event()
-            done.record(stream)
-        return [done] * len(waits)
+            self.exchange(moves, _FG if zstream is not None else _ALL)
+        if zstream is not None:
+            with torch.cuda.stream(zstream):
+                self.exchange(moves, _Z)
 
 
 class DistTransport:
     """torch.distributed point-to-point (NCCL between GPUs, gloo on CPU)."""
 
-    def __init__(self, planes, w, rank, group=None):
+    def __init__(self, planes, w, rank, group=None, zgroup=None):
+        """zgroup: a second process group (its own NCCL communicator and
+        stream) for exchanging Z blocks off the step chain, or None."""
         import torch.distributed as dist
         self.dist = dist
         self.planes = planes
         self.w = w
         self.rank = rank
         self.group = group
+        self.zgroup = zgroup
 
-    def exchange(self, moves):
+    def exchange(self, moves, keys=_ALL, group=None):
         dist = self.dist
+        group = self.group if group is None else group
         # NCCL moves device tensors directly; a gloo group (CPU tests, or
         # several ranks sharing one GPU) stages device blocks through host
         # memory
-        staged = dist.get_backend(self.group) == "gloo"
+        staged = dist.get_backend(group) == "gloo"
         ops, back = [], []
         for (b, src, dst) in moves:
             if src == self.rank:
-                for t in _block_views(self.planes, b, self.w):
-                    ops.append(dist.P2POp(dist.isend, t.cpu() if staged and t.is_cuda else t, dst, self.group))
+                for t in _block_views(self.planes, b, self.w, keys):
+                    ops.append(dist.P2POp(dist.isend, t.cpu() if staged and t.is_cuda else t, dst, group))
             elif dst == self.rank:
-                for t in _block_views(self.planes, b, self.w):
+                for t in _block_views(self.planes, b, self.w, keys):
                     if staged and t.is_cuda:
                         h = t.new_empty(t.shape, device="cpu")
                         back.append((t, h))
                         t = h
-                    ops.append(dist.P2POp(dist.irecv, t, src, self.group))
+                    ops.append(dist.P2POp(dist.irecv, t, src, group))
         if ops:
             for wk in dist.batch_isend_irecv(ops):
                 wk.wait()
         for t, h in back:
             t.copy_(h)
 
-    def exchange_async(self, moves, waits, stream):
-        """exchange() ordered on ``stream``: the stream first waits for this
-        rank's boundary groups (``waits[0]``); NCCL's stream waits on it, and
-        wait() makes it wait for the transfers, so the returned event marks
-        the received blocks ready without a host synchronisation.  (gloo
-        stages through host memory; the device-to-host copies synchronise.)"""
+    def exchange_on(self, moves, stream, zstream=None):
+        """exchange() ordered on ``stream``: NCCL's stream waits on it (it
+        already waits for this rank's end groups) and wait() makes it wait
+        for the transfers, so the next step's end groups see the received
+        blocks without a host synchronisation.  With ``zstream`` (and the Z
+        process group) the Z blocks go on that stream through their own
+        communicator.  (gloo stages through host memory; its device-to-host
+        copies synchronise.)"""
         import torch
         with torch.cuda.stream(stream):
-            for e in waits[0]:
-                stream.wait_event(e)
-            self.exchange(moves)
-            done = torch.cuda.Event()
-            done.record(stream)
-        return [done]
+            self.exchange(moves, _FG if zstream is not None else _ALL)
+        if zstream is not None:
+            with torch.cuda.stream(zstream):
+                self.exchange(moves, _Z, self.zgroup)
 
 
 def gather_blocks(sched, k_final=0):
@@ -187,6 +195,13 @@ def run_ranks(devs, sched, transport, cfg, allreduce=None, wave=None):
     return sweeps, total, big, converged
 
 
+def split_z_default():
+    """Exchange Z blocks on their own stream / communicator (HZG_SPLIT_Z=0:
+    one exchange for all planes)."""
+    import os
+    return os.environ.get("HZG_SPLIT_Z", "1") != "0"
+
+
 def rank_groups(npairs, ngroups=None):
     """Contiguous position groups [(p0, pn), ...] of one rank's slot range
     for the per-rank wavefront (same rule as the single-GPU sweep graph,
@@ -202,26 +217,28 @@ def rank_groups(npairs, ngroups=None):
 
 
 class Wavefront:
-    """Streams and the group split of the per-rank wavefront.
+    """Group split and exchange stream of the per-rank wavefront.
 
     Rank r's slot range is cut into G contiguous position groups, each on
-    its own stream.  Group g of step k+1 waits only for groups g-1, g, g+1
-    of step k on the same rank (a block moves by at most one position per
-    step); the two end groups also wait for the block exchange of step k,
-    which itself waits only for the end groups of step k (the blocks that
-    change owner sit at the ends of a range).  So the Grammian and
-    postmultiply streaming of some groups overlaps the latency-bound inner
-    solves of others, and the NCCL exchange overlaps the interior groups,
-    with no host synchronisation inside a sweep.  Per-pair work is the
-    same as the serialised schedule, so results stay bitwise equal."""
+    its own stream (hzg_wave_step, one library call per step).  Group g of
+    step k+1 waits only for groups g-1, g, g+1 of step k on the same rank
+    (a block moves by at most one position per step); the two end groups
+    also wait for the block exchange of step k, which itself waits only for
+    the end groups of step k (the blocks that change owner sit at the ends
+    of a range).  So the Grammian and postmultiply streaming of some groups
+    overlaps the latency-bound inner solves of others, and the NCCL
+    exchange overlaps the interior groups, with no host synchronisation
+    inside a sweep.  Per-pair work is that of the serialised schedule, so
+    results stay bitwise equal."""
 
-    def __init__(self, devs, npairs, ngroups=None):
-        """npairs: slot-range length of every rank in ``devs``."""
+    def __init__(self, devs, npairs, ngroups=None, split_z=False):
+        """npairs: slot-range length of every rank in ``devs``; split_z:
+        exchange Z blocks on a second stream (zcomm), off the step chain."""
         import torch
         self.torch = torch
-        self.groups = [rank_groups(np_, ngroups) for np_ in npairs]
-        self.streams = [[torch.cuda.Stream(device=d.device) for _ in gr] for d, gr in zip(devs, self.groups)]
+        self.groups = [len(rank_groups(np_, ngroups)) for np_ in npairs]
         self.comm = torch.cuda.Stream(device=devs[0].device)
+        self.zcomm = torch.cuda.Stream(device=devs[0].device) if split_z else None
 
 
 def sweep_ranks(devs, sched, transport, allreduce=None, wave=None):
@@ -253,35 +270,12 @@ def sweep_ranks(devs, sched, transport, allreduce=None, wave=None):
 
 
 def _sweep_wavefront(devs, sched, transport, wave):
-    torch = wave.torch
-    main = torch.cuda.current_stream(devs[0].device)
-    start = torch.cuda.Event()
-    start.record(main)                   # after init / the previous rescale
-    prev = [[start] * len(gr) for gr in wave.groups]
-    xdone = [start] * len(devs)
     for k in range(sched.steps):
-        cur = []
-        for r, d in enumerate(devs):
-            evs = []
-            G = len(wave.groups[r])
-            for g, (p0, pn) in enumerate(wave.groups[r]):
-                s = wave.streams[r][g]
-                for h in (g - 1, g, g + 1):
-                    if 0 <= h < G:
-                        s.wait_event(prev[r][h])
-                if g == 0 or g == G - 1:
-                    s.wait_event(xdone[r])
-                d.run_pairs(k, p0, pn, s)
-                e = torch.cuda.Event()
-                e.record(s)
-                evs.append(e)
-            cur.append(evs)
-        xdone = transport.exchange_async(sched.moves(k), [(evs[0], evs[-1]) for evs in cur], wave.comm)
-        prev = cur
-    for r in range(len(devs)):
-        for e in prev[r]:
-            main.wait_event(e)
-        main.wait_event(xdone[r])
+        for d, g in zip(devs, wave.groups):
+            d.wave_step(k, g, wave.comm, wave.zcomm)
+        transport.exchange_on(sched.moves(k), wave.comm, wave.zcomm)
+    for d in devs:
+        d.wave_join(wave.comm, wave.zcomm)
 
 
 class PartitionedGsvd:
@@ -321,7 +315,10 @@ class PartitionedGsvd:
                 raise ValueError("distributed solve needs world size %d for %d blocks" % (self.nranks, self.nblk))
             dev = DeviceGsvd(planes, cfg, epsn=epsn, schedule=self.sched.colpairs(self.rank, w))
             self.devs = [dev]
-            self.transport = DistTransport(dict(planes, Zr=dev.Zr, Zi=dev.Zi), w, self.rank)
+            # the Z exchange gets its own communicator (and NCCL stream) so
+            # it never queues ahead of the next step's F, G exchange
+            zgroup = dist.new_group(list(range(world))) if wavefront and split_z_default() else None
+            self.transport = DistTransport(dict(planes, Zr=dev.Zr, Zi=dev.Zi), w, self.rank, zgroup=zgroup)
 
             cdev = "cpu" if dist.get_backend() == "gloo" else dev.device
 
@@ -334,7 +331,8 @@ class PartitionedGsvd:
         ranks = range(self.nranks) if comm is None else [self.rank]
         self.wave = None
         if wavefront and torch.cuda.is_available():
-            self.wave = Wavefront(self.devs, [self.sched.ranges[r][1] - self.sched.ranges[r][0] for r in ranks])
+            self.wave = Wavefront(self.devs, [self.sched.ranges[r][1] - self.sched.ranges[r][0] for r in ranks],
+                                  split_z=split_z_default())
         self.sweeps = self.total = self.big = 0
         self.converged = False
 
@@ -370,8 +368,12 @@ class PartitionedGsvd:
         # step-wise driving: 3 kernels per step (per position group with the
         # wavefront), plus the counter fold and the Z rescale per sweep, per
         # rank driven by this process
-        g = sum(len(gr) for gr in self.wave.groups) if self.wave is not None else len(self.devs)
-        return self.sched.steps * 3 * g + 2 * len(self.devs), len(self.devs) + 5
+        g = sum(self.wave.groups) if self.wave is not None else len(self.devs)
+        per_step = 3
+        if self.wave is not None and os.environ.get("HZG_WAVE_DEFER_Z", "0") not in ("", "0") and \
+                os.environ.get("HZG_DEFER_Z", "1") != "0" and not self.cfg.exact:
+            per_step = 4            # the deferred Z postmultiply is a 4th kernel per group and step
+        return self.sched.steps * per_step * g + 2 * len(self.devs), len(self.devs) + 5
 
     def close(self):
         for d in self.devs:

@@ -167,6 +167,16 @@ class DeviceGsvd:
         s = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
         _native.check(self.lib.hzg_run_pairs(self.ctx, step, p0, pn, s), self.ctx, "run_pairs")
 
+    def wave_step(self, step, groups, comm=None, zcomm=None):
+        """Step ``step`` as ``groups`` position groups on library streams,
+        ordered against the exchange streams ``comm`` (F, G and, without
+        ``zcomm``, Z blocks) and ``zcomm`` (Z blocks) (hzg_wave_step)."""
+        _native.check(self.lib.hzg_wave_step(self.ctx, step, groups, _sptr(comm), _sptr(zcomm)), self.ctx,
+                      "wave_step")
+
+    def wave_join(self, comm=None, zcomm=None):
+        _native.check(self.lib.hzg_wave_join(self.ctx, _sptr(comm), _sptr(zcomm)), self.ctx, "wave_join")
+
     def finalize(self, n0=None, mF0=None, mG0=None, sort=True):
         """Final rescale, unborder, sort; returns device output tensors."""
         torch = self.torch
@@ -184,6 +194,10 @@ class DeviceGsvd:
                                             _ptr(out["Zi"]), _ptr(out["sigmaF"]), _ptr(out["sigmaG"]),
                                             _ptr(out["sigma"])), self.ctx, "finalize")
         return out
+
+
+def _sptr(stream):
+    return ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
 
 
 def _planes_of(m):

@@ -310,12 +310,48 @@ def test_block_partitioned_wavefront_bitwise(n, ranks, groups, monkeypatch):
         monkeypatch.setenv("HZG_GROUPS", groups)
     wave = solve_blocks(F, G, cfg, ranks)
     serial = solve_blocks(F, G, cfg, ranks, wavefront=False)
-    for r in (wave, serial):
+    # deferred Z postmultiply on its own streams, Z blocks exchanged apart
+    monkeypatch.setenv("HZG_WAVE_DEFER_Z", "1")
+    wave_defer = solve_blocks(F, G, cfg, ranks)
+    monkeypatch.setenv("HZG_SPLIT_Z", "0")
+    wave_defer1 = solve_blocks(F, G, cfg, ranks)
+    for r in (wave, serial, wave_defer, wave_defer1):
         assert r.workers == ranks
         assert (r.sweeps, r.total_transforms, r.big_transforms) == (one.sweeps, one.total_transforms,
                                                                     one.big_transforms)
         for a, b in ((r.sigma, one.sigma), (r.U.re, one.U.re), (r.V.re, one.V.re), (r.Z.re, one.Z.re)):
             assert np.array_equal(a, b)
+
+
+def test_run_pairs_split_equals_run_steps():
+    """hzg_run_pairs over a split of every step's pairs (two streams,
+    synchronised per step) gives bitwise the planes of hzg_run_steps."""
+    import torch
+    n, w = 512, 16
+    g = O.gaussian_stream(5, 2 * n * n)
+    Fr = torch.from_numpy(g[: n * n].reshape(n, n)).cuda()     # (cols, rows): column-major n x n
+    Gr = torch.from_numpy(g[n * n:].reshape(n, n)).cuda()
+    cfg = hz.SolverConfig(block_width=w)
+    outs = []
+    for split in (False, True):
+        planes = {"Fr": Fr.clone(), "Gr": Gr.clone(), "Fi": None, "Gi": None}
+        dev = hz.DeviceGsvd(planes, cfg)
+        dev.init()
+        s2 = torch.cuda.Stream()
+        npairs = n // w // 2
+        for k in range(n // w - 1):
+            if split:
+                torch.cuda.synchronize()
+                dev.run_pairs(k, 0, 5)
+                dev.run_pairs(k, 5, npairs - 5, s2)
+                torch.cuda.synchronize()
+            else:
+                dev.run_steps(k, 1)
+        torch.cuda.synchronize()
+        outs.append((planes["Fr"].cpu(), planes["Gr"].cpu(), dev.Zr.cpu()))
+        dev.close()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("name", ["genpair256_w16", "gauss200_w16", "corpus64_real_w16", "gauss1024"])
@@ -355,8 +391,9 @@ def test_fused_postgram_bitwise_equals_unfused(name, monkeypatch):
 
 def test_wavefront_groups_bitwise_invariant(monkeypatch):
     """The sweep graph's circle-position groups (streams overlapping the
-    steps of neighbouring groups) must not change a single bit: same
-    solve with 1, 2, 4 and 8 groups (n = 1024, 32 pairs per step)."""
+    steps of neighbouring groups) and the deferred Z postmultiply must not
+    change a single bit: same solve with 1, 2, 4 and 8 groups, with and
+    without the deferral (n = 1024, 32 pairs per step)."""
     g = O.gaussian_stream(91, 2 * 1024 * 1024)
     F = g[: 1024 * 1024].reshape((1024, 1024), order="F")
     G = g[1024 * 1024:].reshape((1024, 1024), order="F")
@@ -365,6 +402,11 @@ def test_wavefront_groups_bitwise_invariant(monkeypatch):
     for groups in ("1", "2", "4", "8"):
         monkeypatch.setenv("HZG_GROUPS", groups)
         runs.append(hz.solve(F, G, cfg))
+    # the Z postmultiply on the step chain instead of its own streams
+    monkeypatch.setenv("HZG_DEFER_Z", "0")
+    runs.append(hz.solve(F, G, cfg))
+    monkeypatch.setenv("HZG_GROUPS", "1")
+    runs.append(hz.solve(F, G, cfg))
     for r in runs[1:]:
         assert (r.sweeps, r.total_transforms, r.big_transforms) == \
             (runs[0].sweeps, runs[0].total_transforms, runs[0].big_transforms)

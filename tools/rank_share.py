@@ -9,7 +9,7 @@ shape).  The slowest rank's sweep time bounds the R-GPU sweep from below
 interior groups), so F_sweep / max_r(t_r) estimates strong scaling on R
 B200s where only one GPU is available.
 
-usage: python tools/rank_share.py N R[,R...] [wave|serial] [sweeps]
+usage: python tools/rank_share.py N R[,R...] [wave|serial|timed|vtimed] [sweeps]
 """
 import os
 import sys
@@ -27,13 +27,8 @@ class NullTransport:
     def exchange(self, moves):
         pass
 
-    def exchange_async(self, moves, waits, stream):
-        with torch.cuda.stream(stream):
-            for e in waits[0]:
-                stream.wait_event(e)
-            done = torch.cuda.Event()
-            done.record(stream)
-        return [done]
+    def exchange_on(self, moves, stream, zstream=None):
+        pass
 
 
 def main():
@@ -51,6 +46,22 @@ def main():
     Fsw = bench.flops_per_sweep(n, n, n, w)
     cfg = hz.SolverConfig(block_width=w, max_outer_sweeps=100)
     for R in Rs:
+        if mode == "vtimed":   # R virtual ranks with real block exchange, per-rank kernel times
+            job = D.PartitionedGsvd({"Fr": F0.clone(), "Gr": G0.clone(), "Fi": None, "Gi": None}, cfg, R,
+                                    wavefront=False)
+            job.init()
+            job.sweep()
+            for d in job.devs:
+                d.set_timing(True)
+                d.kernel_times(reset=True)
+            job.sweep()
+            for r, d in enumerate(job.devs):
+                kt = d.kernel_times()
+                print(f"n={n} R={R} rank {r} (real exchange): " + "  ".join(
+                    f"{k} {v[0] / max(1, v[1]) * 1e3:.1f} us" for k, v in kt.items()), flush=True)
+            job.close()
+            del job
+            continue
         sched = D.BlockSchedule(n // w, R)
         worst = 0.0
         for r in sorted({0, R // 2, R - 1}):
@@ -58,23 +69,40 @@ def main():
             dev = hz.DeviceGsvd({"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}, cfg, epsn=D.epsn_of(cfg, n),
                                 schedule=sched.colpairs(r, w))
             lo, hi = sched.ranges[r]
-            wave = D.Wavefront([dev], [hi - lo]) if mode == "wave" else None
+            wave = D.Wavefront([dev], [hi - lo], split_z=D.split_z_default()) if mode == "wave" else None
             dev.init()
             D.sweep_ranks([dev], sched, NullTransport(), None, wave)   # warm-up sweep
-            times = []
+            if mode == "timed":   # isolated per-kernel times (serialised, synchronous)
+                dev.set_timing(True)
+                dev.kernel_times(reset=True)
+                D.sweep_ranks([dev], sched, NullTransport(), None, None)
+                kt = dev.kernel_times()
+                dev.set_timing(False)
+                print(f"n={n} R={R} rank {r}: " + "  ".join(
+                    f"{k} {v[0] / max(1, v[1]) * 1e3:.1f} us" for k, v in kt.items()), flush=True)
+            times, hs = [], []
             for _ in range(nsw):
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                D.sweep_ranks([dev], sched, NullTransport(), None, wave)
+                h0 = time.perf_counter()
+                if wave is not None:
+                    D._sweep_wavefront([dev], sched, NullTransport(), wave)
+                else:
+                    for k in range(sched.steps):
+                        dev.run_steps(k, 1)
+                hs.append(time.perf_counter() - h0)   # host time to issue the sweep's steps
+                _, big = dev.collect()
+                if big:
+                    dev.rescale_z()
                 e1.record()
                 torch.cuda.synchronize()
                 times.append(e0.elapsed_time(e1) / 1e3)
             t = sorted(times)[len(times) // 2]
             worst = max(worst, t)
-            g = len(wave.groups[0]) if wave else 1
-            print(f"n={n} R={R} rank {r}: {hi - lo} pairs/step, {g} groups, {mode}: sweep {t * 1e3:.1f} ms",
-                  flush=True)
+            g = wave.groups[0] if wave else 1
+            print(f"n={n} R={R} rank {r}: {hi - lo} pairs/step, {g} groups, {mode}: sweep {t * 1e3:.1f} ms "
+                  f"(host issue {min(hs) * 1e3:.1f} ms)", flush=True)
             dev.close()
             del dev, Fw, Gw
         print(f"n={n} R={R} {mode}: slowest rank {worst * 1e3:.1f} ms/sweep -> "
