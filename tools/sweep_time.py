@@ -1,0 +1,42 @@
+"""Device sweep time of the bench workload (no e2e / roofline passes), for
+quick A/B of HZG_* knobs: python tools/sweep_time.py [n] [warmup] [timed]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bench
+import paper_1909_00101_b200 as hz
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+W = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+K = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+
+
+class A:
+    pass
+
+
+a = A()
+a.n, a.kind, a.seed, a.w = n, "gauss", 7, 16
+F0, G0, _ = bench.gen_pair(a, torch, torch.device("cuda"))
+dev = hz.DeviceGsvd({"Fr": F0, "Gr": G0, "Fi": None, "Gi": None}, hz.SolverConfig(block_width=16, max_outer_sweeps=100))
+dev.init()
+for _ in range(W):
+    dev.sweep()
+clk = bench.ClockSampler(0)
+torch.cuda.synchronize()
+clk.start()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(K):
+    dev.sweep()
+e1.record()
+torch.cuda.synchronize()
+c = clk.stop()
+ms = e0.elapsed_time(e1) / K
+tf = bench.flops_per_sweep(n, n, n, 16) / (ms / 1e3) / 1e12
+knobs = " ".join(f"{k}={v}" for k, v in sorted(os.environ.items()) if k.startswith("HZG_"))
+print(f"n={n} {knobs or 'default'}: {ms:.1f} ms/sweep {tf:.2f} TF/s sm {c['sm_mhz']} MHz -> {tf / c['sm_mhz'] * 1e3:.2f} TF/s/GHz",
+      flush=True)
