@@ -29,13 +29,15 @@ import os
 
 import numpy as np
 
-from .strategies import circle_positions, slot_ranges
+from .strategies import circle_positions, slot_ranges, weighted_slot_ranges
 
 
 class BlockSchedule:
     """Circle-position schedule of nblk blocks over nranks ranks."""
 
-    def __init__(self, nblk, nranks):
+    def __init__(self, nblk, nranks, end_weight=None):
+        """end_weight: share of an end rank relative to an interior rank
+        (None: HZG_END_WEIGHT or the default, see end_weight_default)."""
         if nblk < 2 or nblk % 2:
             raise ValueError("need an even number of blocks")
         if nranks < 1 or nranks > nblk // 2:
@@ -44,7 +46,8 @@ class BlockSchedule:
         self.nranks = nranks
         self.steps = nblk - 1
         self.pos = circle_positions(nblk)            # (steps, nblk/2, 2), (min, max)
-        self.ranges = slot_ranges(nblk // 2, nranks)
+        ew = end_weight_default(nblk // 2, nranks) if end_weight is None else end_weight
+        self.ranges = weighted_slot_ranges(nblk // 2, nranks, ew)
         owner = np.empty((self.steps, nblk), dtype=np.int64)
         for r, (lo, hi) in enumerate(self.ranges):
             for k in range(self.steps):
@@ -193,6 +196,18 @@ def run_ranks(devs, sched, transport, cfg, allreduce=None, wave=None):
             converged = True
             break
     return sweeps, total, big, converged
+
+
+def end_weight_default(npos, nranks):
+    """Relative share of the two end ranks (HZG_END_WEIGHT overrides).
+    Measured on the per-rank share at n = 16384 (profiles/r01_rank_share.txt):
+    with 64 pairs per rank (8 ranks) 0.65 balances the end ranks' slower
+    inner solves (728 -> 667 ms per sweep); with 128 (4 ranks) equal ranges
+    are best."""
+    e = os.environ.get("HZG_END_WEIGHT")
+    if e:
+        return float(e)
+    return 0.65 if nranks >= 3 and npos / nranks <= 64 else 1.0
 
 
 def split_z_default():

@@ -164,6 +164,30 @@ def slot_ranges(npos, nranks):
     return out
 
 
+def weighted_slot_ranges(npos, nranks, end_weight=1.0):
+    """Contiguous circle-position ranges [lo, hi) per rank with the two end
+    ranks weighted by ``end_weight`` relative to the interior ranks (every
+    rank keeps at least one position).  The positions next to the ends of
+    the circle ordering need more inner sweeps per pair, so
+    giving their ranks fewer pairs balances the per-step time; the pairs
+    and per-pair work are unchanged, so results do not depend on it."""
+    if nranks < 3 or end_weight == 1.0:
+        return slot_ranges(npos, nranks)
+    wts = [end_weight] + [1.0] * (nranks - 2) + [end_weight]
+    tot = sum(wts)
+    cuts = [0]
+    acc = 0.0
+    for r in range(nranks - 1):
+        acc += wts[r]
+        cuts.append(int(round(npos * acc / tot)))
+    cuts.append(npos)
+    for r in range(1, nranks):                # at least one position per rank
+        cuts[r] = max(cuts[r], cuts[r - 1] + 1)
+    for r in range(nranks - 1, 0, -1):
+        cuts[r] = min(cuts[r], cuts[r + 1] - 1)
+    return [(cuts[r], cuts[r + 1]) for r in range(nranks)]
+
+
 def owner_of_blocks(nblk, nranks):
     """owner[k][b]: rank holding block b during ME step k (circle positions,
     contiguous position ranges per rank)."""

@@ -98,9 +98,10 @@ def test_local_transport_matches_single_process(nblk, world):
         assert torch.equal(planes[0][key], ref[key])
 
 
-def test_schedule_moves_per_rank_and_step():
-    for nblk, world in ((64, 2), (1024, 8), (2048, 8)):
-        sched = BlockSchedule(nblk, world)
+@pytest.mark.parametrize("end_weight", [1.0, 0.6])
+def test_schedule_moves_per_rank_and_step(end_weight):
+    for nblk, world in ((64, 2), (1024, 8), (2048, 8), (96, 5)):
+        sched = BlockSchedule(nblk, world, end_weight=end_weight)
         for k in range(sched.steps):
             mv = sched.moves(k)
             out_per_rank = np.bincount([s for (_, s, _) in mv], minlength=world)
@@ -118,5 +119,30 @@ def test_colpairs_cover_every_pair_once_per_sweep():
         for k in range(sched.steps):
             for c0, c1 in cp[k]:
                 assert c0 < c1
+                seen.add((c0 // w, c1 // w))
+    assert len(seen) == nblk * (nblk - 1) // 2
+
+
+def test_weighted_slot_ranges_partition():
+    from paper_1909_00101_b200.strategies import weighted_slot_ranges
+    for npos in range(1, 70):
+        for world in range(1, npos + 1):
+            for f in (0.1, 0.6, 1.0, 1.7):
+                r = weighted_slot_ranges(npos, world, f)
+                assert r[0][0] == 0 and r[-1][1] == npos and len(r) == world
+                assert all(lo < hi for lo, hi in r)
+                assert all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+    r = weighted_slot_ranges(512, 8, 0.6)
+    assert r[0][1] - r[0][0] < r[1][1] - r[1][0] and r[-1][1] - r[-1][0] == r[0][1] - r[0][0]
+
+
+def test_weighted_schedule_covers_every_pair():
+    nblk, world, w = 40, 4, 8
+    sched = BlockSchedule(nblk, world, end_weight=0.5)
+    seen = set()
+    for r in range(world):
+        cp = sched.colpairs(r, w)
+        for k in range(sched.steps):
+            for c0, c1 in cp[k]:
                 seen.add((c0 // w, c1 // w))
     assert len(seen) == nblk * (nblk - 1) // 2
