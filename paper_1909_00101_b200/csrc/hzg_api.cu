@@ -614,6 +614,26 @@ int hzg_init_fgz(hzg_ctx* c) {
   return HZG_OK;
 }
 
+// first pair of position group g of G (g = G: npairs).  The two end groups
+// hold the circle positions whose pairs need the most inner sweeps; with
+// HZG_GROUP_END_WEIGHT = f they get f times an interior group's share
+// (default 1: equal groups).
+static int group_cut(int npairs, int G, int g) {
+  static double f = -1.0;
+  if (f < 0) {
+    const char* e = std::getenv("HZG_GROUP_END_WEIGHT");
+    f = e ? std::max(0.05, std::atof(e)) : 1.0;
+  }
+  if (g <= 0) return 0;
+  if (g >= G) return npairs;
+  if (G < 3 || f == 1.0 || npairs < 4 * G) return (int)((int64_t)npairs * g / G);
+  const double tot = 2 * f + (G - 2);
+  const double acc = f + (g - 1);
+  int cut = (int)std::lround(npairs * acc / tot);
+  // every group keeps at least one pair
+  return std::min(std::max(cut, g), npairs - (G - g));
+}
+
 static int choose_groups(const hzg_ctx* c) {
   if (!c->wavefront) return 1;
   // measured without per-kernel events (bench.py, HZG_GROUPS sweep): 8
@@ -721,7 +741,7 @@ static int build_graph(hzg_ctx* c) {
       // the inner solve of step st overwrites the transforms the deferred
       // Z postmultiply of step st - 2 (same pairs) reads
       if (dz && st >= 2) cudaStreamWaitEvent(s, zev[(st & 1) * G + g], 0);
-      const int p0 = (int)((int64_t)c->npairs * g / G), p1 = (int)((int64_t)c->npairs * (g + 1) / G);
+      const int p0 = group_cut(c->npairs, G, g), p1 = group_cut(c->npairs, G, g + 1);
       rc = launch_step(c, st, s, c->timing ? &c->tev[((size_t)st * G + g) * 4] : nullptr, p0, p1 - p0, dz,
                        dz ? idone[g] : nullptr);
       cudaEventRecord(stepev[(st & 1) * G + g], s);
@@ -879,7 +899,7 @@ int hzg_wave_step(hzg_ctx* c, int32_t step, int32_t groups, void* comm, void* zc
     }
     // transforms of step - 2 (same buffer) read by its deferred Z postmultiply
     if (dz && step - 2 >= c->wfirst) cudaStreamWaitEvent(s, zev[(step & 1) * G + g], 0);
-    const int p0 = (int)((int64_t)c->npairs * g / G), p1 = (int)((int64_t)c->npairs * (g + 1) / G);
+    const int p0 = group_cut(c->npairs, G, g), p1 = group_cut(c->npairs, G, g + 1);
     int rc = launch_step(c, step, s, nullptr, p0, p1 - p0, dz, dz ? idone[g] : nullptr);
     if (rc) return fail(c, rc, "step launch");
     cudaEventRecord(sev[(step & 1) * G + g], s);
