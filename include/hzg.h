@@ -171,6 +171,17 @@ int hzg_test_fastmath(int64_t n, uint64_t seed, int64_t* counts4);
  *   hzg_op_postmultiply   -> postmultiply                   (blocked.py:370-381, :220-250), Y in place
  *   hzg_op_rescale        -> rescale_z                      (blocked.py:384-401, :253-295), in place;
  *                            Z has mZ rows, sigF/sigG/sig written when final != 0 */
+/* Householder R factor, in place, of the m x nc column-major matrix A
+ * (m >= nc; Ai NULL for real), with column pivoting when pivot != 0 (the
+ * column of largest remaining norm at each step, ties to the lowest
+ * index; jpvt[nc] is permuted alongside), bitwise the reference's
+ * _k_qr_rfactor (blocked.py:97-217) as used by preprocess_tall
+ * (blocked.py:405-428).  *result = the reference's return value: 1 when
+ * a column vanished or a diagonal fell below tol_scale times its column's
+ * entry norm, else 0.  Device pointers; synchronous on `stream`. */
+int hzg_op_qr_rfactor(int64_t m, int32_t nc, int32_t is_complex, int32_t pivot, double tol_scale, double* Ar,
+                      double* Ai, int64_t* jpvt, int32_t* result, void* stream);
+
 int hzg_op_grammian(int64_t m, int32_t w, int32_t is_complex, int32_t compensated, const double* Yr,
                     const double* Yi, double* Ar, double* Ai, void* stream);
 int hzg_op_cholesky_upper(int32_t tw, int32_t is_complex, double* Ar, double* Ai, void* stream);

@@ -11,7 +11,8 @@ from .core import (GsvdResult, MatrixPlanePair, ProblemPair, border_pair, read_m
                    write_matrix)
 from .errors import (DeviceError, FileFormatError, HzgsvdError, NotPositiveDefiniteError,
                      ProtocolError, RankError)
-from .ops import cholesky_upper, form_grammians, postmultiply, qr_shorten, rescale_z, run_distributed
+from .ops import (cholesky_upper, form_grammians, postmultiply, preprocess_tall, qr_shorten, rescale_z,
+                  run_distributed)
 from .solver import DeviceGsvd, clear_cache, gsvd_1x1, gsvd_blocked, solve, upload_bordered
 from .strategies import (CommMapping, StrategyTable, block_moves, circle_positions, comm_mapping,
                          dump_table, gen_table, validate_table)
@@ -24,5 +25,5 @@ __all__ = [
     "NotPositiveDefiniteError", "ProtocolError", "RankError", "DeviceGsvd", "gsvd_1x1", "gsvd_blocked",
     "solve", "upload_bordered", "CommMapping", "StrategyTable", "block_moves", "circle_positions",
     "comm_mapping", "dump_table", "gen_table", "validate_table", "cholesky_upper", "form_grammians",
-    "postmultiply", "qr_shorten", "rescale_z", "run_distributed", "clear_cache",
+    "postmultiply", "qr_shorten", "rescale_z", "run_distributed", "clear_cache", "preprocess_tall",
 ]

@@ -26,7 +26,7 @@ class HzgConfig(ctypes.Structure):
 EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_init_fgz", "hzg_sweep",
            "hzg_run_steps", "hzg_run_pairs", "hzg_wave_step", "hzg_wave_join", "hzg_collect", "hzg_rescale_z", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
            "hzg_step_counters", "hzg_debug_phases", "hzg_launch_counts", "hzg_op_grammian",
-           "hzg_op_cholesky_upper", "hzg_op_qr_shorten", "hzg_op_postmultiply", "hzg_op_rescale", "hzg_test_fastmath", "hzg_last_error",
+           "hzg_op_cholesky_upper", "hzg_op_qr_shorten", "hzg_op_qr_rfactor", "hzg_op_postmultiply", "hzg_op_rescale", "hzg_test_fastmath", "hzg_last_error",
            "hzg_destroy")
 
 _lib = None
@@ -88,6 +88,8 @@ def load(path=LIB_PATH):
         L.hzg_op_cholesky_upper.restype = ctypes.c_int
         L.hzg_op_qr_shorten.argtypes = [I64, I32, I32, P, P, P, P, P]
         L.hzg_op_qr_shorten.restype = ctypes.c_int
+        L.hzg_op_qr_rfactor.argtypes = [I64, I32, I32, I32, ctypes.c_double, P, P, P, P, P]
+        L.hzg_op_qr_rfactor.restype = ctypes.c_int
         L.hzg_op_postmultiply.argtypes = [I64, I32, I32, P, P, P, P, P]
         L.hzg_op_postmultiply.restype = ctypes.c_int
         L.hzg_op_rescale.argtypes = [I64, I64, I64, I32, I32, I32] + [P] * 6 + [I64, P, P, P, P]

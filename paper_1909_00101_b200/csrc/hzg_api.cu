@@ -1136,6 +1136,22 @@ struct DevBuf {
 };
 }  // namespace
 
+int hzg_op_qr_rfactor(int64_t m, int32_t nc, int32_t is_complex, int32_t pivot, double tol_scale, double* Ar,
+                      double* Ai, int64_t* jpvt, int32_t* result, void* stream) {
+  if (m < 1 || nc < 1 || m < nc || !Ar || (is_complex && !Ai) || !jpvt || !result) return HZG_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  DevBuf scr, fl;
+  if (scr.alloc((size_t)(2 * nc + 4) * 8) != cudaSuccess || fl.alloc(8) != cudaSuccess) return HZG_CUDA;
+  int32_t h[2] = {0, 0};
+  if (cudaMemsetAsync(fl.p, 0, 8, s) != cudaSuccess) return HZG_CUDA;
+  if (launch_qr_rfactor(Ar, Ai, m, nc, is_complex, pivot, tol_scale, jpvt, (double*)scr.p, (int32_t*)fl.p, s))
+    return HZG_CUDA;
+  if (cudaMemcpyAsync(h, fl.p, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return HZG_CUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return HZG_CUDA;
+  *result = (h[0] || h[1]) ? 1 : 0;
+  return HZG_OK;
+}
+
 int hzg_op_grammian(int64_t m, int32_t w, int32_t cplx, int32_t comp, const double* Yr, const double* Yi, double* Ar,
                     double* Ai, void* stream) {
   if (m < 1 || w < 1 || !Yr || !Ar || (cplx && (!Yi || !Ai))) return HZG_INVALID;

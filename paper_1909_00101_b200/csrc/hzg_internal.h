@@ -85,6 +85,12 @@ int launch_postmult_exact(const Plane& F, const Plane& G, const Plane& Z, const 
 int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const StepPairs& sp, int step, int w,
                          int cplx, const InnerOut& io, cudaStream_t s, int mat0 = 0, int nmats = 3);
 
+// Column-pivoted Householder R factor of an m x nc column-major matrix in
+// place (hzg_tall.cu; _k_qr_rfactor, blocked.py:97-217); flags[0] = column
+// vanished, flags[1] = rank test failed (caller zeroes both)
+int launch_qr_rfactor(double* Ar, double* Ai, int64_t m, int nc, int cplx, int pivot, double tol_scale,
+                      int64_t* jpvt, double* scratch, int32_t* flags, cudaStream_t s);
+
 // Fused postmultiply of step `step` (F and G) and Grammian partials of step
 // `step + 1` along chains of circle positions (hzg_dmma.cu, 2w = 32, real).
 struct PostGramTables {

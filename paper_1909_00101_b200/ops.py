@@ -1,7 +1,8 @@
 """Single block operations of the reference's public API on the device.
 
-form_grammians, cholesky_upper, qr_shorten, postmultiply and rescale_z keep
-the reference's signatures and results (pkg/src/hzgsvd/blocked.py:328-401)
+form_grammians, cholesky_upper, qr_shorten, postmultiply, rescale_z and
+preprocess_tall keep the reference's signatures and results
+(pkg/src/hzgsvd/blocked.py:328-428)
 and run the same reference-order kernels the solver uses (bitwise the
 reference), through the C ABI (include/hzg.h, hzg_op_*).  run_distributed
 (distsim.py:147) keeps its signature and runs the block-partitioned
@@ -99,6 +100,54 @@ def qr_shorten(Yp, Yq):
                                                    _stream(torch)), None,
                   "rank-deficient block columns in the QR shortening")
     return _host(Rr, Ri)
+
+
+def qr_rfactor(Ar, Ai, pivot, jpvt, tol_scale):
+    """In-place Householder R factor of device planes (column-major (cols,
+    rows) float64 tensors; Ai None for real), with column pivoting into the
+    int64 device tensor jpvt; returns the reference's flag (blocked.py:97-217:
+    1 = a column vanished or a diagonal fell below tol_scale x its entry
+    norm)."""
+    torch = _torch()
+    nc, m = Ar.shape
+    res = ctypes.c_int32(0)
+    _native.check(_native.load().hzg_op_qr_rfactor(m, nc, int(Ai is not None), int(bool(pivot)), float(tol_scale),
+                                                    _p(Ar), _p(Ai), _p(jpvt), ctypes.byref(res), _stream(torch)),
+                  None, "qr_rfactor")
+    return res.value
+
+
+def preprocess_tall(F, G):
+    """Shorten a tall pair to square via two column-pivoted QR
+    factorizations on the device (blocked.py:405-428): returns (F'', G'',
+    piv) with column k of the shortened problem = original column piv[k];
+    a Z'' of the shortened pair maps back by Z[piv[k], :] = Z''[k, :].
+    Bitwise the reference (same fma order, same pivot ties)."""
+    from .config import EPS
+    from .errors import RankError
+    torch = _torch()
+    n = F.cols
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def planes(M):
+        re = torch.from_numpy(np.ascontiguousarray(M.re.T, dtype=np.float64)).to(dev)
+        im = torch.from_numpy(np.ascontiguousarray(M.im.T, dtype=np.float64)).to(dev) if M.is_complex else None
+        return re, im
+
+    Fr, Fi = planes(F)
+    jp1 = torch.arange(n, dtype=torch.int64, device=dev)
+    if qr_rfactor(Fr, Fi, True, jp1, n * EPS) != 0:
+        raise RankError("numerically rank-deficient F in the preprocessing")
+    Gr, Gi = planes(G)
+    Gr = Gr[jp1].contiguous()                        # G[:, jp1]
+    Gi = Gi[jp1].contiguous() if Gi is not None else None
+    jp2 = torch.arange(n, dtype=torch.int64, device=dev)
+    if qr_rfactor(Gr, Gi, True, jp2, n * EPS) != 0:
+        raise RankError("numerically rank-deficient G in the preprocessing")
+    Fpp = MatrixPlanePair.from_dense(_host(Fr[jp2, :n], Fi[jp2, :n] if Fi is not None else None))
+    Gpp = MatrixPlanePair.from_dense(_host(Gr[:, :n], Gi[:, :n] if Gi is not None else None))
+    piv = jp1[jp2].cpu().numpy()
+    return Fpp, Gpp, piv
 
 
 def postmultiply(Yp, Yq, Ztilde):
