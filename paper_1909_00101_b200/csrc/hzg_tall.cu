@@ -9,12 +9,15 @@
 // choice, the reflector dot w = v^H a_c and the update a_c -= v w); the
 // parallelism is across the remaining columns, and each step k is a short
 // sequence of launches:
-//   k_tall_norms   squared norms of the columns k..nc-1 over rows k..m-1
-//   k_tall_pivot   first column of largest norm (ties to the lowest index,
-//                  NaN never wins), column swap, jpvt / entry-norm swap
-//   k_tall_reflect the reflector of column k (one thread: the vn chain)
-//   k_tall_apply   w and the update of every column c > k
-//   k_tall_close   R(k,k) = alpha, zeros below it
+//   k_tall_cols<0>        squared norms of the columns k..nc-1 over rows k..m-1
+//   k_tall_pivot_reflect  first column of largest norm (ties to the lowest
+//                         index, NaN never wins), column swap, jpvt /
+//                         entry-norm swap; the reflector of column k (one
+//                         thread: the vn chain)
+//   k_tall_cols<2>        w and the update of every column c > k
+//   k_tall_close          R(k,k) = alpha, zeros below it
+// (k_tall_cols<1>: the entry norms, once).  The chains read their columns
+// through shared-memory tiles so the global loads are coalesced.
 // then k_tall_final: the rank test against the entry norms and the phase
 // fix that makes the diagonal real and nonnegative.  The matrix is m x nc
 // column-major with leading dimension m (real and imaginary planes).
@@ -30,6 +33,34 @@ namespace hzg {
 namespace {
 
 constexpr int kTallThreads = 128;
+constexpr int kU = 8;  // loads issued ahead of each run of dependent fmas
+
+// s = fma(x, x, s) (and fma(y, y, s)) over rows [x0, m), the reference's
+// order; the loads of kU rows are issued before their fmas so the chain runs
+// at fma latency instead of load latency (same operations, same order)
+template <bool CPLX>
+__device__ __forceinline__ double sq_chain(const double* __restrict__ xr, const double* __restrict__ xi, int64_t x0,
+                                           int64_t m, double s) {
+  int64_t x = x0;
+  for (; x + kU <= m; x += kU) {
+    double r[kU], i[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      r[u] = xr[x + u];
+      if (CPLX) i[u] = xi[x + u];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      s = fma(r[u], r[u], s);
+      if (CPLX) s = fma(i[u], i[u], s);
+    }
+  }
+  for (; x < m; ++x) {
+    s = fma(xr[x], xr[x], s);
+    if (CPLX) s = fma(xi[x], xi[x], s);
+  }
+  return s;
+}
 
 struct TallArgs {
   double* Ar;
@@ -42,35 +73,6 @@ struct TallArgs {
   double* scal;    // alr, ali, beta
   int32_t* flag;   // [0]: 1 when a column vanished (the reference returns 1 at once)
 };
-
-template <bool CPLX>
-__global__ void __launch_bounds__(kTallThreads) k_tall_innorm(TallArgs a) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= a.nc) return;
-  const double* xr = a.Ar + (int64_t)c * a.m;
-  const double* xi = CPLX ? a.Ai + (int64_t)c * a.m : nullptr;
-  double s = 0.0;
-  for (int64_t x = 0; x < a.m; ++x) {
-    s = fma(xr[x], xr[x], s);
-    if (CPLX) s = fma(xi[x], xi[x], s);
-  }
-  a.innorm[c] = sqrt(s);
-}
-
-// squared norms over rows k.. of columns k + [0, cnt)
-template <bool CPLX>
-__global__ void __launch_bounds__(kTallThreads) k_tall_norms(TallArgs a, int k, int cnt) {
-  const int c = k + blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= k + cnt || *a.flag) return;
-  const double* xr = a.Ar + (int64_t)c * a.m;
-  const double* xi = CPLX ? a.Ai + (int64_t)c * a.m : nullptr;
-  double s = 0.0;
-  for (int64_t x = k; x < a.m; ++x) {
-    s = fma(xr[x], xr[x], s);
-    if (CPLX) s = fma(xi[x], xi[x], s);
-  }
-  a.cn[c] = s;
-}
 
 // one CTA: pivot choice and column swap (pivot) and the reflector of
 // column k (thread 0; its norm is the squared norm already computed for the
@@ -161,45 +163,10 @@ __global__ void __launch_bounds__(1024) k_tall_pivot_reflect(TallArgs a, int k, 
   const double ali = -(phi * normx);
   vr[k] -= alr;
   if (CPLX) vi[k] -= ali;
-  double vn = 0.0;
-  for (int64_t x = k; x < a.m; ++x) {
-    vn = fma(vr[x], vr[x], vn);
-    if (CPLX) vn = fma(vi[x], vi[x], vn);
-  }
+  const double vn = sq_chain<CPLX>(vr, vi, k, a.m, 0.0);
   a.scal[0] = alr;
   a.scal[1] = ali;
   a.scal[2] = 2.0 / vn;
-}
-
-template <bool CPLX>
-__global__ void __launch_bounds__(kTallThreads) k_tall_apply(TallArgs a, int k) {
-  const int c = k + 1 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= a.nc || *a.flag) return;
-  const double beta = a.scal[2];
-  const double* vr = a.Ar + (int64_t)k * a.m;
-  const double* vi = CPLX ? a.Ai + (int64_t)k * a.m : nullptr;
-  double* xr = a.Ar + (int64_t)c * a.m;
-  double* xi = CPLX ? a.Ai + (int64_t)c * a.m : nullptr;
-  double wr = 0.0, wi = 0.0;
-  for (int64_t x = k; x < a.m; ++x) {
-    // w += conj(v_x) * a_x
-    wr = fma(vr[x], xr[x], wr);
-    if (CPLX) {
-      wr = fma(vi[x], xi[x], wr);
-      wi = fma(vr[x], xi[x], fma(-vi[x], xr[x], wi));
-    }
-  }
-  wr *= beta;
-  wi *= beta;
-  for (int64_t x = k; x < a.m; ++x) {
-    // a_x -= v_x * w
-    double r = fma(-vr[x], wr, xr[x]);
-    if (CPLX) {
-      r = fma(vi[x], wi, r);
-      xi[x] = fma(-vr[x], wi, fma(-vi[x], wr, xi[x]));
-    }
-    xr[x] = r;
-  }
 }
 
 template <bool CPLX>
@@ -248,16 +215,171 @@ __global__ void __launch_bounds__(kTallThreads) k_tall_final(TallArgs a, double 
   }
 }
 
+// Column chains with coalesced loads: a warp owns 32 consecutive columns
+// (one per lane) and walks the rows in tiles of 32: the tile is read column
+// by column with lanes along the rows (coalesced), transposed through shared
+// memory, and every lane then runs its own column's fma chain over the tile
+// in row order — the reference's order.  MODE 0: squared norms over rows
+// k.. of columns [c0, c0 + cnt) into cn; MODE 1: entry norms (rows 0..)
+// into innorm; MODE 2: the reflector of column k applied to the columns
+// [c0, c0 + cnt) (w = beta v^H a_c, then a_c -= v w, written back through
+// the same tiles).
+constexpr int kTile = 32;
+constexpr int kWarps = 2;  // 64 columns per CTA (static shared memory < 48 KB for complex)
+constexpr int kColThreads = kWarps * 32;
+
+// one tile of rows [x0, x0 + 32) of the warp's columns into registers: lane
+// l holds row x0 + l of every column (coalesced along the rows)
+template <bool CPLX>
+__device__ __forceinline__ void tile_load(const TallArgs& a, int cbase, int ncols, int64_t x0, int l, double* nr,
+                                          double* ni) {
+  const bool ok = x0 + l < a.m;
+#pragma unroll
+  for (int j = 0; j < kTile; ++j) {
+    const bool on = ok && j < ncols;
+    const int64_t e = (int64_t)(cbase + j) * a.m + x0 + l;
+    nr[j] = on ? a.Ar[e] : 0.0;
+    if (CPLX) ni[j] = on ? a.Ai[e] : 0.0;
+  }
+}
+
+template <bool CPLX>
+__device__ __forceinline__ void tile_put(double (*tr)[kTile + 1], double (*ti)[kTile + 1], int l, const double* nr,
+                                         const double* ni) {
+#pragma unroll
+  for (int j = 0; j < kTile; ++j) {
+    tr[l][j] = nr[j];
+    if (CPLX) ti[l][j] = ni[j];
+  }
+}
+
+template <bool CPLX, int MODE>
+__global__ void __launch_bounds__(kColThreads) k_tall_cols(TallArgs a, int k, int c0, int cnt) {
+  __shared__ double tr[kWarps][kTile][kTile + 1];
+  __shared__ double ti[CPLX ? kWarps : 1][kTile][kTile + 1];
+  __shared__ double sv[kWarps][2][kTile];
+  if (MODE != 1 && *a.flag) return;
+  const int wp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int cbase = c0 + (blockIdx.x * kWarps + wp) * 32;
+  if (cbase >= c0 + cnt) return;
+  const int ncols = min(32, c0 + cnt - cbase);
+  const bool active = l < ncols;
+  const int64_t m = a.m;
+  const int64_t xs = MODE == 1 ? 0 : k;
+  const double* vr = a.Ar + (int64_t)k * m;
+  const double* vi = CPLX ? a.Ai + (int64_t)k * m : nullptr;
+  double (*TR)[kTile + 1] = tr[wp];
+  double (*TI)[kTile + 1] = ti[CPLX ? wp : 0];
+  double nr[kTile], ni[CPLX ? kTile : 1];
+  double s = 0.0, wr = 0.0, wi = 0.0;
+  double pv_r = 0.0, pv_i = 0.0;
+  // pass 1: the chains, the next tile's loads in flight under this tile's fmas
+  tile_load<CPLX>(a, cbase, ncols, xs, l, nr, ni);
+  if (MODE == 2 && xs + l < m) {
+    pv_r = vr[xs + l];
+    if (CPLX) pv_i = vi[xs + l];
+  }
+  for (int64_t x0 = xs; x0 < m; x0 += kTile) {
+    const int rows = m - x0 < kTile ? (int)(m - x0) : kTile;
+    tile_put<CPLX>(TR, TI, l, nr, ni);
+    if (MODE == 2) {
+      sv[wp][0][l] = pv_r;
+      if (CPLX) sv[wp][1][l] = pv_i;
+    }
+    __syncwarp();
+    if (x0 + kTile < m) {
+      tile_load<CPLX>(a, cbase, ncols, x0 + kTile, l, nr, ni);
+      if (MODE == 2 && x0 + kTile + l < m) {
+        pv_r = vr[x0 + kTile + l];
+        if (CPLX) pv_i = vi[x0 + kTile + l];
+      }
+    }
+    if (active) {
+      for (int r = 0; r < rows; ++r) {
+        const double xr = TR[r][l];
+        const double xi = CPLX ? TI[r][l] : 0.0;
+        if (MODE != 2) {
+          s = fma(xr, xr, s);
+          if (CPLX) s = fma(xi, xi, s);
+        } else {
+          const double pr = sv[wp][0][r];
+          const double pi = CPLX ? sv[wp][1][r] : 0.0;
+          // w += conj(v_x) * a_x
+          wr = fma(pr, xr, wr);
+          if (CPLX) {
+            wr = fma(pi, xi, wr);
+            wi = fma(pr, xi, fma(-pi, xr, wi));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (MODE == 0) {
+    if (active) a.cn[cbase + l] = s;
+    return;
+  }
+  if (MODE == 1) {
+    if (active) a.innorm[cbase + l] = sqrt(s);
+    return;
+  }
+  const double beta = a.scal[2];
+  wr *= beta;
+  wi *= beta;
+  // pass 2: a_x -= v_x * w through the same tiles, written back coalesced
+  tile_load<CPLX>(a, cbase, ncols, xs, l, nr, ni);
+  if (xs + l < m) {
+    pv_r = vr[xs + l];
+    if (CPLX) pv_i = vi[xs + l];
+  }
+  for (int64_t x0 = xs; x0 < m; x0 += kTile) {
+    const int rows = m - x0 < kTile ? (int)(m - x0) : kTile;
+    tile_put<CPLX>(TR, TI, l, nr, ni);
+    sv[wp][0][l] = pv_r;
+    if (CPLX) sv[wp][1][l] = pv_i;
+    __syncwarp();
+    if (x0 + kTile < m) {
+      tile_load<CPLX>(a, cbase, ncols, x0 + kTile, l, nr, ni);
+      if (x0 + kTile + l < m) {
+        pv_r = vr[x0 + kTile + l];
+        if (CPLX) pv_i = vi[x0 + kTile + l];
+      }
+    }
+    if (active) {
+      for (int r = 0; r < rows; ++r) {
+        const double pr = sv[wp][0][r];
+        double xr = fma(-pr, wr, TR[r][l]);
+        if (CPLX) {
+          const double pi = sv[wp][1][r];
+          xr = fma(pi, wi, xr);
+          TI[r][l] = fma(-pr, wi, fma(-pi, wr, TI[r][l]));
+        }
+        TR[r][l] = xr;
+      }
+    }
+    __syncwarp();
+    if (l < rows) {
+      for (int j = 0; j < ncols; ++j) {
+        a.Ar[(int64_t)(cbase + j) * m + x0 + l] = TR[l][j];
+        if (CPLX) a.Ai[(int64_t)(cbase + j) * m + x0 + l] = TI[l][j];
+      }
+    }
+    __syncwarp();
+  }
+}
+
 inline int blocks_for(int64_t n) { return (int)((n + kTallThreads - 1) / kTallThreads); }
+inline int col_blocks(int64_t n) { return (int)((n + kColThreads - 1) / kColThreads); }
 
 template <bool CPLX>
 int run_qr_rfactor(TallArgs a, int pivot, double tol_scale, int32_t* bad, cudaStream_t s) {
-  k_tall_innorm<CPLX><<<blocks_for(a.nc), kTallThreads, 0, s>>>(a);
+  k_tall_cols<CPLX, 1><<<col_blocks(a.nc), kColThreads, 0, s>>>(a, 0, 0, a.nc);
   for (int k = 0; k < a.nc; ++k) {
     const int cnt = pivot ? a.nc - k : 1;
-    k_tall_norms<CPLX><<<blocks_for(cnt), kTallThreads, 0, s>>>(a, k, cnt);
+    k_tall_cols<CPLX, 0><<<col_blocks(cnt), kColThreads, 0, s>>>(a, k, k, cnt);
     k_tall_pivot_reflect<CPLX><<<1, 1024, 0, s>>>(a, k, pivot);
-    if (k + 1 < a.nc) k_tall_apply<CPLX><<<blocks_for(a.nc - k - 1), kTallThreads, 0, s>>>(a, k);
+    if (k + 1 < a.nc)
+      k_tall_cols<CPLX, 2><<<col_blocks(a.nc - k - 1), kColThreads, 0, s>>>(a, k, k + 1, a.nc - k - 1);
     k_tall_close<CPLX><<<blocks_for(a.m - k), kTallThreads, 0, s>>>(a, k);
   }
   k_tall_final<CPLX><<<blocks_for(a.nc), kTallThreads, 0, s>>>(a, tol_scale, bad);
