@@ -723,6 +723,12 @@ static int qr_rfactor(double* Ar, double* Ai, int64_t m, int nc, int cplx, int p
 }
 
 /* exported: the QR shortening of blocked.py:487-500 on an m x tw stack (in place), R -> outR/outI (tw x tw) */
+/* _k_qr_rfactor itself (blocked.py:97-217), in place, with the caller's
+ * pivot flag and jpvt: the building block of preprocess_tall (:405-428) */
+int hzo_qr_rfactor(int64_t m, int nc, int cplx, int pivot, double tol_scale, double* Ar, double* Ai, int64_t* jpvt) {
+  return qr_rfactor(Ar, Ai, m, nc, cplx, pivot, jpvt, tol_scale);
+}
+
 int hzo_qr_shorten(int64_t m, int tw, int cplx, double* Sr, double* Si, double* outR, double* outI) {
   int64_t* jpvt = (int64_t*)malloc(sizeof(int64_t) * tw);
   for (int k = 0; k < tw; ++k) jpvt[k] = k;

@@ -72,6 +72,8 @@ def lib():
         L.hzo_grammian.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    P, P, ctypes.c_int64, ctypes.c_int64, P, P]
         L.hzo_qr_shorten.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, P, P, P, P]
+        L.hzo_qr_rfactor.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                     P, P, P]
         L.hzo_tree_reduce.argtypes = [P, ctypes.c_int64]
         L.hzo_tree_reduce.restype = ctypes.c_double
         _lib = L
@@ -111,6 +113,31 @@ def gen_table(kind, n):
 def tree_reduce(x):
     x = np.ascontiguousarray(x, dtype=np.float64)
     return lib().hzo_tree_reduce(_p(x), x.size)
+
+
+def preprocess_tall(F, G):
+    """Restatement of preprocess_tall (blocked.py:405-428) on dense numpy
+    F (m x n), G (p x n): returns (F'', G'', piv) or raises OracleError
+    (code 1) like the reference's RankError."""
+    n = F.shape[1]
+    EPSN = n * 2.0 ** -52
+
+    def qr(A):
+        cplx = np.iscomplexobj(A)
+        Ar = np.array(np.real(A), dtype=np.float64, order="F", copy=True)
+        Ai = np.array(np.imag(A), dtype=np.float64, order="F", copy=True) if cplx else np.zeros_like(Ar, order="F")
+        jp = np.arange(n, dtype=np.int64)
+        rc = lib().hzo_qr_rfactor(A.shape[0], n, int(cplx), 1, EPSN, _p(Ar), _p(Ai), _p(jp))
+        R = Ar[:n, :] + 1j * Ai[:n, :] if cplx else Ar[:n, :].copy()
+        return rc, R, jp
+
+    rc, RF, jp1 = qr(F)
+    if rc:
+        raise OracleError(1, "numerically rank-deficient F in the preprocessing")
+    rc, RG, jp2 = qr(G[:, jp1])
+    if rc:
+        raise OracleError(1, "numerically rank-deficient G in the preprocessing")
+    return RF[:, jp2], RG, jp1[jp2]
 
 
 def cholesky_upper(A):

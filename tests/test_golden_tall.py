@@ -38,3 +38,22 @@ def test_tall_golden_consistent(name):
     for A, B in ((Fpp, Fp), (Gpp, Gp)):
         ga, gb = A.conj().T @ A, B.conj().T @ B
         assert np.max(np.abs(ga - gb)) <= 1e-12 * np.max(np.abs(gb))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_preprocess_tall_bitwise_vs_reference(name):
+    """The oracle's restatement (hzo_qr_rfactor, hzg_oracle.c) reproduces
+    the reference's preprocess_tall bitwise, errors included."""
+    from oracle import oracle as O
+    d = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    cplx = bool(d["cplx"])
+    F = d["F_re"] + 1j * d["F_im"] if cplx else d["F_re"]
+    G = d["G_re"] + 1j * d["G_im"] if cplx else d["G_re"]
+    if str(d["error"]):
+        with pytest.raises(O.OracleError, match="rank-deficient %s" % str(d["error"])):
+            O.preprocess_tall(F, G)
+        return
+    Fpp, Gpp, piv = O.preprocess_tall(F, G)
+    assert np.array_equal(piv, d["piv"])
+    assert np.array_equal(np.real(Fpp), d["Fpp_re"]) and np.array_equal(np.imag(Fpp), d["Fpp_im"])
+    assert np.array_equal(np.real(Gpp), d["Gpp_re"]) and np.array_equal(np.imag(Gpp), d["Gpp_im"])

@@ -57,3 +57,21 @@ def test_preprocess_tall_then_solve_recovers_sigma():
     r_short = hz.solve(Fpp, Gpp, cfg)
     rel = np.abs(r_short.sigma - r_tall.sigma) / r_tall.sigma
     assert rel.max() < 64 * n * 2.2e-16
+
+
+@pytest.mark.parametrize("m,n,p,cplx", [(300, 200, 240, False), (260, 160, 200, True), (97, 97, 97, False)])
+def test_preprocess_tall_bitwise_vs_oracle_random(m, n, p, cplx):
+    """Larger seeded pairs than the golden cases: device vs the oracle's
+    restatement (itself pinned to the reference's golden vectors)."""
+    import paper_1909_00101_b200 as hz
+    from oracle import oracle as O
+    g = O.gaussian_stream(m + n + p, 2 * (m + p) * n)
+    F = g[: m * n].reshape((m, n), order="F")
+    G = g[m * n: (m + p) * n].reshape((p, n), order="F")
+    if cplx:
+        F = F + 1j * g[(m + p) * n: (2 * m + p) * n].reshape((m, n), order="F")
+        G = G + 1j * g[(2 * m + p) * n:].reshape((p, n), order="F")
+    Fo, Go, po = O.preprocess_tall(F, G)
+    Fpp, Gpp, piv = hz.preprocess_tall(hz.MatrixPlanePair.from_dense(F), hz.MatrixPlanePair.from_dense(G))
+    assert np.array_equal(piv, po)
+    assert np.array_equal(Fpp.to_dense(), Fo) and np.array_equal(Gpp.to_dense(), Go)
