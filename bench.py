@@ -421,19 +421,24 @@ def main():
     tot_k = sum(v[0] for v in kt.values())
     post_gbs = bpl["postmult"] / (avg["postmult"] / 1e3) / 1e9
     gram_gbs = bpl["grammian"] / (avg["grammian"] / 1e3) / 1e9
-    traffic = None
+    traffic = gram_traffic = None
     traffic_file = os.path.join(ROOT, "profiles", "traffic_w%d_n%d.json" % (w, n))
-    if os.path.exists(traffic_file):
+    if os.path.exists(traffic_file):   # ncu --set full capture of the same kernels (committed)
         with open(traffic_file) as fh:
-            traffic = json.load(fh).get("postmult_dram_bytes_per_launch")
+            tj = json.load(fh)
+        traffic = tj.get("postmult_dram_bytes_per_launch")
+        gram_traffic = tj.get("grammian_dram_bytes_per_launch")
     roofline = {"kernel": "k_post_ws (postmultiply of F, G, Z block pairs; the dominant HBM-bound kernel)",
                 "bound": "hbm", "achieved": post_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": post_gbs / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": post_gbs / hbm_peak, "traffic": traffic,
+                "traffic_note": ("DRAM bytes per launch, ncu --set full (profiles/traffic_w%d_n%d.json)" % (w, n))
+                if traffic else None,
+                "peak_source": peak_src,
                 "bytes_per_launch": bpl["postmult"], "avg_launch_ms": avg["postmult"],
                 "measured": "isolated: sweep 1 of this pair, one launch per outer step covering all %d pairs, "
                             "CUDA events on the launch stream" % (n // w // 2),
                 "grammian": {"achieved": gram_gbs, "frac": gram_gbs / hbm_peak, "bytes_per_launch": bpl["grammian"],
-                             "avg_launch_ms": avg["grammian"]},
+                             "avg_launch_ms": avg["grammian"], "traffic": gram_traffic},
                 "inner": {"avg_launch_ms": avg["inner"], "bound": "latency (dependent FP64 div/sqrt chains + "
                                                                  "one CTA barrier per inner step)"},
                 "kernel_time_shares_isolated": {k: v[0] / tot_k for k, v in kt.items()} if tot_k else {},
