@@ -474,3 +474,25 @@ def test_dmma_mode_w32_within_tolerance(name):
     m = gsvd_metrics(c["F"], c["G"], r)
     assert m["resF"] <= 4 * nn * EPS and m["resG"] <= 4 * nn * EPS
     assert m["orthU"] <= 32 * nn * EPS and m["orthV"] <= 32 * nn * EPS
+
+
+@pytest.mark.parametrize("groups", ["8", "16"])
+def test_sweep_graph_repeatable_many_groups(groups, monkeypatch):
+    """Race check of the concurrent sweep graph (position groups, deferred Z
+    on low-priority streams, double-buffered transforms): three solves of
+    the same n = 2048 pair with fresh contexts are bitwise identical."""
+    monkeypatch.setenv("HZG_GROUPS", groups)
+    n = 2048
+    g = O.gaussian_stream(4242, 2 * n * n)
+    F = g[: n * n].reshape((n, n), order="F")
+    G = g[n * n:].reshape((n, n), order="F")
+    cfg = hz.SolverConfig(block_width=16, max_outer_sweeps=6)
+    runs = []
+    for _ in range(3):
+        hz.clear_cache()
+        runs.append(hz.solve(F, G, cfg))
+    for r in runs[1:]:
+        assert (r.sweeps, r.total_transforms, r.big_transforms) == \
+            (runs[0].sweeps, runs[0].total_transforms, runs[0].big_transforms)
+        for a, b in ((r.sigma, runs[0].sigma), (r.Z.re, runs[0].Z.re), (r.U.re, runs[0].U.re)):
+            assert np.array_equal(a, b)
