@@ -393,8 +393,9 @@ def main():
     # warm: two calls, so the pinned host blocks of two results (the one the
     # caller still holds while the next call runs, and the next one) are in
     # torch's caching host allocator before the timed calls
-    api()
-    api()
+    w1 = api()
+    w2 = api()
+    del w1, w2
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
