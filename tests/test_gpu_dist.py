@@ -62,3 +62,14 @@ def test_solve_blocks_multiprocess_wavefront_groups():
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), 512, 16, out, "3"), nprocs=2, join=True)
     assert out["ok"] and out["workers"] == 2 and out["rank1_none"]
+
+
+def test_solve_blocks_multiprocess_deferred_z_split_exchange(monkeypatch):
+    """Deferred Z postmultiply in the per-rank wavefront with the Z blocks
+    exchanged through a second process group (HZG_WAVE_DEFER_Z=1,
+    HZG_SPLIT_Z default): two processes, 2 groups per rank."""
+    monkeypatch.setenv("HZG_WAVE_DEFER_Z", "1")
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), 512, 16, out, "2"), nprocs=2, join=True)
+    assert out["ok"] and out["workers"] == 2 and out["rank1_none"]
