@@ -211,10 +211,14 @@ def end_weight_default(npos, nranks):
 
 
 def split_z_default():
-    """Exchange Z blocks on their own stream / communicator (HZG_SPLIT_Z=0:
-    one exchange for all planes)."""
-    import os
-    return os.environ.get("HZG_SPLIT_Z", "1") != "0"
+    """Exchange Z blocks on their own stream / communicator: only useful
+    with the deferred Z postmultiply (HZG_WAVE_DEFER_Z=1), so on by default
+    only then (HZG_SPLIT_Z overrides); otherwise one exchange (one NCCL
+    communicator) carries every plane."""
+    e = os.environ.get("HZG_SPLIT_Z")
+    if e is not None:
+        return e != "0"
+    return os.environ.get("HZG_WAVE_DEFER_Z", "0") not in ("", "0")
 
 
 def rank_groups(npairs, ngroups=None):
