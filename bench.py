@@ -208,7 +208,7 @@ def run_reference(a):
     osteps = n // a.w - 1
     line = {"metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * tot_t / a.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": workload_name(a), "n": n, "block_width": a.w,
                        "sample": "%d outer steps of sweep 1 in total (of %d per sweep)" % (tot_s, osteps)},
@@ -469,7 +469,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
             "warmup": W, "ms_per_step": ms_max / a.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak",
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated on the GPU)",
             "config": {"workload": workload_name(a), "n": n, "block_width": w,
                        "step": "one outer sweep (%d outer steps x %d block pairs) after %d warm-up sweeps"
