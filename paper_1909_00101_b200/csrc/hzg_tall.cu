@@ -253,6 +253,27 @@ __device__ __forceinline__ void tile_put(double (*tr)[kTile + 1], double (*ti)[k
   }
 }
 
+// one row of a lane's chain: s += |a_x|^2 (MODE 0, 1) or w += conj(v_x) a_x
+// (MODE 2), the reference's fma order
+template <bool CPLX, int MODE>
+__device__ __forceinline__ void chain_row(double (*TR)[kTile + 1], double (*TI)[kTile + 1], double (*sv)[kTile],
+                                          int r, int l, double& s, double& wr, double& wi) {
+  const double xr = TR[r][l];
+  const double xi = CPLX ? TI[r][l] : 0.0;
+  if (MODE != 2) {
+    s = fma(xr, xr, s);
+    if (CPLX) s = fma(xi, xi, s);
+  } else {
+    const double pr = sv[0][r];
+    const double pi = CPLX ? sv[1][r] : 0.0;
+    wr = fma(pr, xr, wr);
+    if (CPLX) {
+      wr = fma(pi, xi, wr);
+      wi = fma(pr, xi, fma(-pi, xr, wi));
+    }
+  }
+}
+
 template <bool CPLX, int MODE>
 __global__ void __launch_bounds__(kColThreads) k_tall_cols(TallArgs a, int k, int c0, int cnt) {
   __shared__ double tr[kWarps][kTile][kTile + 1];
@@ -295,22 +316,13 @@ __global__ void __launch_bounds__(kColThreads) k_tall_cols(TallArgs a, int k, in
       }
     }
     if (active) {
-      for (int r = 0; r < rows; ++r) {
-        const double xr = TR[r][l];
-        const double xi = CPLX ? TI[r][l] : 0.0;
-        if (MODE != 2) {
-          s = fma(xr, xr, s);
-          if (CPLX) s = fma(xi, xi, s);
-        } else {
-          const double pr = sv[wp][0][r];
-          const double pi = CPLX ? sv[wp][1][r] : 0.0;
-          // w += conj(v_x) * a_x
-          wr = fma(pr, xr, wr);
-          if (CPLX) {
-            wr = fma(pi, xi, wr);
-            wi = fma(pr, xi, fma(-pi, xr, wi));
-          }
-        }
+      if (rows == kTile) {
+        // full tile: unrolled, so the shared-memory reads run ahead of the
+        // dependent fma chain
+#pragma unroll
+        for (int r = 0; r < kTile; ++r) chain_row<CPLX, MODE>(TR, TI, sv[wp], r, l, s, wr, wi);
+      } else {
+        for (int r = 0; r < rows; ++r) chain_row<CPLX, MODE>(TR, TI, sv[wp], r, l, s, wr, wi);
       }
     }
     __syncwarp();
@@ -346,6 +358,7 @@ __global__ void __launch_bounds__(kColThreads) k_tall_cols(TallArgs a, int k, in
       }
     }
     if (active) {
+#pragma unroll 8
       for (int r = 0; r < rows; ++r) {
         const double pr = sv[wp][0][r];
         double xr = fma(-pr, wr, TR[r][l]);
