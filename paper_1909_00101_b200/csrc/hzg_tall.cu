@@ -10,6 +10,8 @@
 // parallelism is across the remaining columns, and each step k is a short
 // sequence of launches:
 //   k_tall_cols<0>        squared norms of the columns k..nc-1 over rows k..m-1
+//                         (step 0; later steps get them from the update
+//                         pass of the previous step, k_tall_cols<2>)
 //   k_tall_pivot_reflect  first column of largest norm (ties to the lowest
 //                         index, NaN never wins), column swap, jpvt /
 //                         entry-norm swap; the reflector of column k (one
@@ -338,6 +340,7 @@ __global__ void __launch_bounds__(kColThreads) k_tall_cols(TallArgs a, int k, in
   const double beta = a.scal[2];
   wr *= beta;
   wi *= beta;
+  s = 0.0;
   // pass 2: a_x -= v_x * w through the same tiles, written back coalesced
   tile_load<CPLX>(a, cbase, ncols, xs, l, nr, ni);
   if (xs + l < m) {
@@ -362,12 +365,20 @@ __global__ void __launch_bounds__(kColThreads) k_tall_cols(TallArgs a, int k, in
       for (int r = 0; r < rows; ++r) {
         const double pr = sv[wp][0][r];
         double xr = fma(-pr, wr, TR[r][l]);
+        double xi = 0.0;
         if (CPLX) {
           const double pi = sv[wp][1][r];
           xr = fma(pi, wi, xr);
-          TI[r][l] = fma(-pr, wi, fma(-pi, wr, TI[r][l]));
+          xi = fma(-pr, wi, fma(-pi, wr, TI[r][l]));
+          TI[r][l] = xi;
         }
         TR[r][l] = xr;
+        // the next step's pivot norm of this column (rows k+1.., updated
+        // values, the reference's order): k_tall_cols<0> folded in
+        if (x0 + r > k) {
+          s = fma(xr, xr, s);
+          if (CPLX) s = fma(xi, xi, s);
+        }
       }
     }
     __syncwarp();
@@ -379,6 +390,7 @@ __global__ void __launch_bounds__(kColThreads) k_tall_cols(TallArgs a, int k, in
     }
     __syncwarp();
   }
+  if (active) a.cn[cbase + l] = s;
 }
 
 inline int blocks_for(int64_t n) { return (int)((n + kTallThreads - 1) / kTallThreads); }
@@ -388,8 +400,11 @@ template <bool CPLX>
 int run_qr_rfactor(TallArgs a, int pivot, double tol_scale, int32_t* bad, cudaStream_t s) {
   k_tall_cols<CPLX, 1><<<col_blocks(a.nc), kColThreads, 0, s>>>(a, 0, 0, a.nc);
   for (int k = 0; k < a.nc; ++k) {
-    const int cnt = pivot ? a.nc - k : 1;
-    k_tall_cols<CPLX, 0><<<col_blocks(cnt), kColThreads, 0, s>>>(a, k, k, cnt);
+    // pivot norms: step 0 here, later steps from the previous update pass
+    if (k == 0) {
+      const int cnt = pivot ? a.nc : 1;
+      k_tall_cols<CPLX, 0><<<col_blocks(cnt), kColThreads, 0, s>>>(a, 0, 0, cnt);
+    }
     k_tall_pivot_reflect<CPLX><<<1, 1024, 0, s>>>(a, k, pivot);
     if (k + 1 < a.nc)
       k_tall_cols<CPLX, 2><<<col_blocks(a.nc - k - 1), kColThreads, 0, s>>>(a, k, k + 1, a.nc - k - 1);

@@ -22,3 +22,19 @@ t0 = time.perf_counter()
 hz.preprocess_tall(Fm, Gm)
 torch.cuda.synchronize()
 print(f"preprocess_tall complex F {m}x{n}, G {n}x{n}: {time.perf_counter() - t0:.3f} s (host in/out included)", flush=True)
+
+# device-only: the column-pivoted R factor of F on resident planes (median of 3)
+from paper_1909_00101_b200 import ops
+ts = []
+for _ in range(3):
+    Fr = torch.from_numpy(np.ascontiguousarray(F.real.T)).cuda()
+    Fi = torch.from_numpy(np.ascontiguousarray(F.imag.T)).cuda()
+    jp = torch.arange(n, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ops.qr_rfactor(Fr, Fi, True, jp, n * 2.0 ** -52)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1) / 1e3)
+print(f"qr_rfactor complex {m}x{n} with pivoting, device only: {sorted(ts)[1]:.3f} s (median of 3)", flush=True)
