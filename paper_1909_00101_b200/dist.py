@@ -210,6 +210,17 @@ def end_weight_default(npos, nranks):
     return 0.65 if nranks >= 3 and npos / nranks <= 64 else 1.0
 
 
+_ZGROUPS = {}
+
+
+def _z_group(dist, world):
+    """The second process group of the split Z exchange, created once per
+    world size (every rank calls this at the same point)."""
+    if world not in _ZGROUPS:
+        _ZGROUPS[world] = dist.new_group(list(range(world)))
+    return _ZGROUPS[world]
+
+
 def split_z_default():
     """Exchange Z blocks on their own stream / communicator: only useful
     with the deferred Z postmultiply (HZG_WAVE_DEFER_Z=1), so on by default
@@ -336,7 +347,7 @@ class PartitionedGsvd:
             self.devs = [dev]
             # the Z exchange gets its own communicator (and NCCL stream) so
             # it never queues ahead of the next step's F, G exchange
-            zgroup = dist.new_group(list(range(world))) if wavefront and split_z_default() else None
+            zgroup = _z_group(dist, world) if wavefront and split_z_default() else None
             self.transport = DistTransport(dict(planes, Zr=dev.Zr, Zi=dev.Zi), w, self.rank, zgroup=zgroup)
 
             cdev = "cpu" if dist.get_backend() == "gloo" else dev.device
