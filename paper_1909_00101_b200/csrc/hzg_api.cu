@@ -639,6 +639,9 @@ static int choose_groups(const hzg_ctx* c) {
   // measured without per-kernel events (bench.py, HZG_GROUPS sweep): 8
   // groups at n = 4096 and n = 16384 (19.0 / 19.4 / 19.6 / 19.6 TFLOP/s for
   // 2 / 4 / 6 / 8 groups at n = 16384)
+  // (n = 4096: 64 groups of 2 pairs save 2-4 ms per sweep but their
+  // ~100k-node graph costs ~0.7 s more to capture and instantiate than a
+  // whole config-4 solve gains; tools/sweep_time.py reports both)
   int g = std::max(1, std::min(8, c->npairs / 16));
   if (const char* e = std::getenv("HZG_GROUPS")) g = std::max(1, std::min(c->npairs, std::atoi(e)));
   return g;

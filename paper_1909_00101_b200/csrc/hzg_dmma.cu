@@ -621,11 +621,11 @@ int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const S
   int64_t mmax = 0;
   const Plane* Y[3] = {&F, &G, &Z};
   for (int q = mat0; q < mat0 + nmats; ++q) mmax = Y[q]->rows > mmax ? Y[q]->rows : mmax;
-  // rows per CTA: the largest of 1024 / 2048 / 4096 that still gives the
-  // launch at least 2 CTAs per SM (fewer, longer CTAs stream better at
-  // n = 16384: 20.33 vs 19.96 TFLOP/s with 4096 vs 1024; at n = 4096 the
-  // small per-group launches need the CTA count); HZG_POST_CHUNK overrides
-  // (multiple of 64).  Row chunking does not change any output bit.
+  // rows per CTA: the largest of 1024 / 2048 / 4096 that still gives a
+  // whole step (all its pairs, whatever the group split) at least 2 CTAs
+  // per SM (fewer, longer CTAs stream better at n = 16384: 20.33 vs 19.96
+  // TFLOP/s with 4096 vs 1024; n = 4096 keeps 1024); HZG_POST_CHUNK
+  // overrides (multiple of 64).  Row chunking does not change any output bit.
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -633,7 +633,7 @@ int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const S
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
   }
   int64_t chunk = 1024;
-  while (chunk < 4096 && (int64_t)sp.pn * ((mmax + 2 * chunk - 1) / (2 * chunk)) * nmats >= 2 * sms) chunk *= 2;
+  while (chunk < 4096 && (int64_t)sp.npairs * ((mmax + 2 * chunk - 1) / (2 * chunk)) * nmats >= 2 * sms) chunk *= 2;
   if (const char* e = std::getenv("HZG_POST_CHUNK")) chunk = std::max(64, std::atoi(e)) / 64 * 64;
   PostParams p{{F, G, Z}, sp, step, io, chunk, mat0};
   switch (2 * w) {
