@@ -48,6 +48,7 @@ typedef struct {
   int32_t shorten_qr;       /* shorten == "qr" */
   double gate_eps;          /* 2**-52 */
   int32_t exact;            /* 1: reference-order Grammian / postmultiply kernels */
+  int32_t split_rows;       /* DMMA Grammian rows per split (multiple of 64); 0 = default geometry */
 } hzg_config;
 
 typedef struct hzg_ctx hzg_ctx;
@@ -71,6 +72,11 @@ int hzg_bind(hzg_ctx* ctx, double* Fr, double* Fi, double* Gr, double* Gi, doubl
  * logical index first).  Used to run a slot range of the ordering on one
  * GPU of a multi-GPU job.  npairs <= n / (2w). */
 int hzg_set_schedule(hzg_ctx* ctx, const int32_t* colpairs, int32_t osteps, int32_t npairs);
+
+/* Rows of the Z plane (default n).  A stripe slab of the reference's
+ * distributed scheme (distsim.py:62-95) owns 2W of the n global columns but
+ * its Z keeps all n_global rows (Z is n_global x 2W).  Before hzg_bind. */
+int hzg_set_z_rows(hzg_ctx* ctx, int64_t zrows);
 
 /* Initial G column scaling and Z0 (synchronous: returns the status). */
 int hzg_init_fgz(hzg_ctx* ctx);
@@ -192,6 +198,36 @@ int hzg_op_postmultiply(int64_t m, int32_t w, int32_t is_complex, double* Yr, do
 int hzg_op_rescale(int64_t mF, int64_t mG, int64_t n, int32_t is_complex, int32_t compensated, int32_t final,
                    double* Fr, double* Fi, double* Gr, double* Gi, double* Zr, double* Zi, int64_t mZ, double* sigF,
                    double* sigG, double* sig, void* stream);
+
+/* ---- multi-GPU data plane (the reference's per-step block
+ * exchange, distsim.py:103-144, re-designed as device-to-device NCCL over
+ * NVLink inside the library).  One process per GPU; each rank's context is
+ * set to its slot range of the circle-position schedule (hzg_set_schedule)
+ * and holds full-size planes (a block lives at its logical column offset).
+ * NCCL is resolved at run time from the process (dlopen). */
+
+/* ncclUniqueId of a new job (rank 0 calls it and broadcasts the bytes). */
+int hzg_comm_unique_id(void* id_out);
+size_t hzg_comm_unique_id_bytes(void);
+/* ncclCommInitRank on ctx's device (collective over the nranks ranks). */
+int hzg_comm_attach(hzg_ctx* ctx, int32_t nranks, int32_t rank, const void* unique_id);
+/* The block moves after every outer step: moves[3q .. 3q+2] = (block,
+ * src rank, dst rank); step k's moves are q in [offsets[k], offsets[k+1]).
+ * Moves not involving this rank are ignored.  osteps must match the
+ * schedule. */
+int hzg_comm_set_moves(hzg_ctx* ctx, const int32_t* moves, const int32_t* offsets, int32_t osteps);
+/* One outer sweep of this rank as ONE captured CUDA graph: its pairs of
+ * every step (position groups), the grouped ncclSend/ncclRecv block
+ * exchange after every step, the counter fold, ncclAllReduce of the
+ * counters and status indicators, the Z rescale gated on the global big
+ * count, ncclAllReduce of its status.  Returns the GLOBAL counters; every
+ * rank returns the same status.  Synchronous (one host sync per sweep). */
+int hzg_dist_sweep(hzg_ctx* ctx, int64_t* total, int64_t* big);
+/* Immediate grouped exchange of whole blocks (e.g. the final gather of
+ * every block to rank 0); synchronous. */
+int hzg_comm_exchange(hzg_ctx* ctx, const int32_t* moves, int32_t count);
+/* Destroy the communicator (hzg_destroy does it too). */
+int hzg_comm_detach(hzg_ctx* ctx);
 
 const char* hzg_last_error(const hzg_ctx* ctx);
 void hzg_destroy(hzg_ctx* ctx);

@@ -311,3 +311,72 @@ def gaussian_stream(seed, count):
     r = np.sqrt(-2.0 * np.log(u[0::2]))
     a = 2.0 * math.pi * u[1::2]
     return r * np.cos(a)
+
+
+# ---------------------------------------------------------------------------
+# deterministic fixture inputs for the north-star configurations (hzo_gen.c).
+# numpy's SIMD log/cos differ between hosts in the last bit (1,680 of 2^20
+# values here vs glibc), so the fixtures regenerate their inputs in C.
+# ---------------------------------------------------------------------------
+
+def gaussian_c(seed, count):
+    """harness.py:66-71 with glibc log/cos (host-independent bytes)."""
+    L = lib()
+    L.hzo_gaussian_fill.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p]
+    out = np.empty(int(count))
+    L.hzo_gaussian_fill(int(seed) % (1 << 64), out.size, _p(out))
+    return out
+
+
+def gen_cond(n, seed):
+    """SURVEY 8(d) config 4 pair (sigma in [1e-8, 1e8]); returns (F, G, sigma_true)."""
+    L = lib()
+    L.hzo_gen_cond.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    F = np.empty((n, n), order="F")
+    G = np.empty((n, n), order="F")
+    s = np.empty(n)
+    if L.hzo_gen_cond(n, int(seed), _p(F), _p(G), _p(s)):
+        raise MemoryError("hzo_gen_cond")
+    return F, G, s
+
+
+NS_CONFIGS = {
+    # name: (BASELINE.json config index, description)
+    "config2": (1, "real 1024 x 1024, iid Gaussian (hzo_gaussian_fill seed 1024), w=16"),
+    "config3": (2, "complex F 3072 x 2048, G 2048 x 2048, iid Gaussian re/im (seeds 31..34), w=16"),
+    "config4": (3, "real 4096 x 4096, sigma = shuffled logspace(-8, 8) (hzo_gen_cond seed 4), w=16, "
+                   "max_outer_sweeps=100"),
+}
+
+
+def ns_inputs(name, scale=1):
+    """Inputs of a north-star fixture: (F, G, cfg kwargs, extra).  `scale`
+    divides every dimension (for quick self-tests of the machinery)."""
+    if name == "config2":
+        n = 1024 // scale
+        g = gaussian_c(1024, 2 * n * n)
+        return (g[: n * n].reshape((n, n), order="F"), g[n * n:].reshape((n, n), order="F"),
+                dict(block_width=16), {})
+    if name == "config3":
+        m, n = 3072 // scale, 2048 // scale
+        F = (gaussian_c(31, m * n) + 1j * gaussian_c(32, m * n)).reshape((m, n), order="F")
+        G = (gaussian_c(33, n * n) + 1j * gaussian_c(34, n * n)).reshape((n, n), order="F")
+        return F, G, dict(block_width=16), {}
+    if name == "config4":
+        n = 4096 // scale
+        F, G, s = gen_cond(n, 4)
+        return F, G, dict(block_width=16, max_outer_sweeps=100), {"sigma_true": np.sort(s)[::-1].copy()}
+    raise KeyError(name)
+
+
+def sha256_planes(*arrays):
+    """SHA-256 over the Fortran-order bytes of real planes (complex arrays
+    contribute their real then imaginary plane)."""
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.asarray(a)
+        parts = (a.real, a.imag) if np.iscomplexobj(a) else (a,)
+        for p in parts:
+            h.update(np.asfortranarray(p, dtype=np.float64).tobytes(order="F"))
+    return h.hexdigest()

@@ -7,13 +7,13 @@ CUDA (libhzg.so, C ABI in include/hzg.h).
 """
 
 from .config import EPS, SolverConfig, SweepStats
-from .core import (GsvdResult, MatrixPlanePair, ProblemPair, border_pair, read_matrix,
-                   write_matrix)
+from .core import GsvdResult, MatrixPlanePair, ProblemPair, border_pair
 from .errors import (DeviceError, FileFormatError, HzgsvdError, NotPositiveDefiniteError,
                      ProtocolError, RankError)
 from .ops import (cholesky_upper, form_grammians, postmultiply, preprocess_tall, qr_shorten, rescale_z,
                   run_distributed)
 from .solver import DeviceGsvd, clear_cache, gsvd_1x1, gsvd_blocked, solve, upload_bordered
+from .stripes import StripeState, exchange_step, partition_stripes
 from .strategies import (CommMapping, StrategyTable, block_moves, circle_positions, comm_mapping,
                          dump_table, gen_table, validate_table)
 
@@ -21,9 +21,10 @@ __version__ = "0.1.0"
 
 __all__ = [
     "EPS", "SolverConfig", "SweepStats", "GsvdResult", "MatrixPlanePair", "ProblemPair", "border_pair",
-    "read_matrix", "write_matrix", "DeviceError", "FileFormatError", "HzgsvdError",
+    "DeviceError", "FileFormatError", "HzgsvdError",
     "NotPositiveDefiniteError", "ProtocolError", "RankError", "DeviceGsvd", "gsvd_1x1", "gsvd_blocked",
     "solve", "upload_bordered", "CommMapping", "StrategyTable", "block_moves", "circle_positions",
     "comm_mapping", "dump_table", "gen_table", "validate_table", "cholesky_upper", "form_grammians",
     "postmultiply", "qr_shorten", "rescale_z", "run_distributed", "clear_cache", "preprocess_tall",
+    "StripeState", "exchange_step", "partition_stripes",
 ]

@@ -20,13 +20,15 @@ class HzgConfig(ctypes.Structure):
     _fields_ = [("variant_id", ctypes.c_int32), ("outer_mm", ctypes.c_int32), ("inner_mm", ctypes.c_int32),
                 ("max_inner_sweeps", ctypes.c_int32), ("max_outer_sweeps", ctypes.c_int32),
                 ("block_width", ctypes.c_int32), ("sorting", ctypes.c_int32), ("fallback_qr", ctypes.c_int32),
-                ("shorten_qr", ctypes.c_int32), ("gate_eps", ctypes.c_double), ("exact", ctypes.c_int32)]
+                ("shorten_qr", ctypes.c_int32), ("gate_eps", ctypes.c_double), ("exact", ctypes.c_int32),
+                ("split_rows", ctypes.c_int32)]
 
 
-EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_init_fgz", "hzg_sweep",
+EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_set_z_rows", "hzg_init_fgz", "hzg_sweep",
            "hzg_run_steps", "hzg_run_pairs", "hzg_wave_step", "hzg_wave_join", "hzg_collect", "hzg_rescale_z", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
            "hzg_step_counters", "hzg_debug_phases", "hzg_launch_counts", "hzg_op_grammian",
-           "hzg_op_cholesky_upper", "hzg_op_qr_shorten", "hzg_op_qr_rfactor", "hzg_op_postmultiply", "hzg_op_rescale", "hzg_test_fastmath", "hzg_last_error",
+           "hzg_op_cholesky_upper", "hzg_op_qr_shorten", "hzg_op_qr_rfactor", "hzg_op_postmultiply", "hzg_op_rescale", "hzg_test_fastmath", "hzg_comm_unique_id", "hzg_comm_unique_id_bytes", "hzg_comm_attach",
+           "hzg_comm_set_moves", "hzg_dist_sweep", "hzg_comm_exchange", "hzg_comm_detach", "hzg_last_error",
            "hzg_destroy")
 
 _lib = None
@@ -52,6 +54,8 @@ def load(path=LIB_PATH):
         L.hzg_bind.restype = ctypes.c_int
         L.hzg_set_schedule.argtypes = [P, P, I32, I32]
         L.hzg_set_schedule.restype = ctypes.c_int
+        L.hzg_set_z_rows.argtypes = [P, I64]
+        L.hzg_set_z_rows.restype = ctypes.c_int
         L.hzg_init_fgz.argtypes = [P]
         L.hzg_init_fgz.restype = ctypes.c_int
         L.hzg_sweep.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -96,6 +100,20 @@ def load(path=LIB_PATH):
         L.hzg_op_rescale.restype = ctypes.c_int
         L.hzg_test_fastmath.argtypes = [I64, ctypes.c_uint64, P]
         L.hzg_test_fastmath.restype = ctypes.c_int
+        L.hzg_comm_unique_id.argtypes = [P]
+        L.hzg_comm_unique_id.restype = ctypes.c_int
+        L.hzg_comm_unique_id_bytes.argtypes = []
+        L.hzg_comm_unique_id_bytes.restype = ctypes.c_size_t
+        L.hzg_comm_attach.argtypes = [P, I32, I32, P]
+        L.hzg_comm_attach.restype = ctypes.c_int
+        L.hzg_comm_set_moves.argtypes = [P, P, P, I32]
+        L.hzg_comm_set_moves.restype = ctypes.c_int
+        L.hzg_dist_sweep.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.hzg_dist_sweep.restype = ctypes.c_int
+        L.hzg_comm_exchange.argtypes = [P, P, I32]
+        L.hzg_comm_exchange.restype = ctypes.c_int
+        L.hzg_comm_detach.argtypes = [P]
+        L.hzg_comm_detach.restype = ctypes.c_int
         L.hzg_last_error.argtypes = [P]
         L.hzg_last_error.restype = ctypes.c_char_p
         L.hzg_destroy.argtypes = [P]
@@ -109,7 +127,7 @@ def make_config(cfg):
     return HzgConfig(cfg.variant_id, int(cfg.outer_kind == "mm"), int(cfg.inner_kind == "mm"),
                      cfg.max_inner_sweeps, cfg.max_outer_sweeps, cfg.block_width, int(bool(cfg.sorting)),
                      int(bool(cfg.fallback_qr)), int(cfg.shorten == "qr"), float(cfg.gate_eps),
-                     int(bool(getattr(cfg, "exact", False))))
+                     int(bool(getattr(cfg, "exact", False))), int(getattr(cfg, "split_rows", 0)))
 
 
 def check(code, ctx=None, what=""):

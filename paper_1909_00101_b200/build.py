@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libhzg.so")
-SOURCES = ["hzg_api.cu", "hzg_kernels.cu", "hzg_inner.cu", "hzg_dmma.cu", "hzg_tall.cu"]
+SOURCES = ["hzg_api.cu", "hzg_kernels.cu", "hzg_inner.cu", "hzg_dmma.cu", "hzg_tall.cu", "hzg_nccl.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -66,7 +66,7 @@ def build(force=False, verbose=False):
             if verbose and msg:
                 sys.stderr.write(msg)
     if force or jobs or _stale(LIB, objs):
-        run([nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda"])
+        run([nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda", "-ldl"])
     return LIB
 
 

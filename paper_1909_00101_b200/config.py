@@ -1,9 +1,16 @@
 """Solver configuration (the reference's SolverConfig, pointwise.py:40-81).
 
-Same fields, defaults, decoding and ValueError behaviour.  One B200-only
-field is added: ``exact`` selects the reference-order Grammian and
-postmultiply kernels (bitwise agreement with the CPU reference) instead of
-the FP64 tensor-core (DMMA) kernels used by default.
+Same fields, defaults, decoding and ValueError behaviour.  Two B200-only
+fields are added:
+
+* ``exact`` selects the reference-order Grammian and postmultiply kernels
+  (bitwise agreement with the CPU reference) instead of the FP64
+  tensor-core (DMMA) kernels used by default;
+* ``split_rows`` (DMMA mode) fixes the rows per Grammian split (a multiple
+  of 64, 0 = the default geometry).  The split geometry sets the summation
+  order of the block Grammians, so it is part of the configuration, not of
+  the environment: results are bitwise reproducible for a given
+  SolverConfig, whatever HZG_* performance variables are set.
 """
 
 from dataclasses import dataclass, field as dc_field
@@ -34,6 +41,7 @@ class SolverConfig:
     shorten: str = "grammian"
     pool: int = 1
     exact: bool = False
+    split_rows: int = 0
     criterion: str = dc_field(init=False, default="C1")
     prescale: bool = dc_field(init=False, default=True)
     compensated: bool = dc_field(init=False, default=False)
@@ -49,6 +57,8 @@ class SolverConfig:
             raise ValueError("shorten must be grammian or qr")
         if self.block_width < 1:
             raise ValueError("block width must be at least 1")
+        if self.split_rows < 0 or self.split_rows % 64:
+            raise ValueError("split_rows must be 0 or a positive multiple of 64")
         self.criterion = "C1" if self.variant_id < 4 else "C2"
         self.prescale = self.variant_id in (0, 1, 4, 5)
         self.compensated = self.variant_id % 2 == 1

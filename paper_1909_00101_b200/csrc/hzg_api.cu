@@ -16,12 +16,14 @@
 
 #include "../../include/hzg.h"
 #include "hzg_internal.h"
+#include "hzg_nccl.h"
 
 using namespace hzg;
 
 struct hzg_ctx {
   int device = 0;
   int64_t mF = 0, mG = 0, n = 0;
+  int64_t zrows = 0;        // rows of Z (n unless hzg_set_z_rows: a stripe slab's Z keeps the global rows)
   int cplx = 0;
   hzg_config cfg{};
   double epsn = 0;
@@ -89,6 +91,19 @@ struct hzg_ctx {
   std::vector<cudaEvent_t> rev;  // [count][4] (hzg_run_steps)
   double kms[3] = {0, 0, 0};
   int64_t kcnt[3] = {0, 0, 0};
+  // multi-GPU data plane (hzg_comm_*, hzg_dist_sweep): this rank's NCCL
+  // communicator, its block moves per step, and the captured rank sweep
+  const hzg::nccl::Api* nc = nullptr;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  std::vector<int32_t> moves;     // (block, src, dst) triples that involve this rank
+  std::vector<int32_t> move_off;  // [osteps + 1] offsets (in triples) per step
+  cudaStream_t xstream = nullptr; // exchange stream of the rank sweep graph
+  std::vector<cudaEvent_t> devents;
+  cudaGraph_t dgraph = nullptr;
+  cudaGraphExec_t dgexec = nullptr;
+  int dgroups = 0;
+  int64_t* d_red = nullptr;       // 8 int64: reduced total, big, any error, not-PD, rank, rescale status
 };
 
 namespace {
@@ -189,22 +204,19 @@ int cuda_fail(hzg_ctx* c, cudaError_t e, const char* where) {
 
 // Grammian split geometry per matrix height (depends on m only, never on
 // the GPU count, so results are GPU-count invariant).
-// rows per Grammian split in DMMA mode: HZG_SPLIT_ROWS fixes them (the
-// fused postmultiply + Grammian needs <= 256); 0 = default geometry
-int64_t split_rows() {
-  const char* e = std::getenv("HZG_SPLIT_ROWS");
-  return e ? std::max<int64_t>(64, std::atoi(e)) / 64 * 64 : 0;
-}
-
-void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
-  const int64_t kSplitRows = split_rows();
+// rows per Grammian split in DMMA mode: hzg_config.split_rows fixes them
+// (the fused postmultiply + Grammian needs <= 256); 0 = default geometry.
+// A configuration field, not an environment variable: it sets the
+// Grammians' summation order, i.e. the result bits.
+void gram_split(int64_t m, bool exact, int64_t split_rows_cfg, int& nsplit, int64_t& chunk) {
+  const int64_t kSplitRows = split_rows_cfg > 0 ? std::max<int64_t>(64, split_rows_cfg) / 64 * 64 : 0;
   if (exact) {
     int64_t P = pow2c(m);
     chunk = std::max<int64_t>(32, std::min<int64_t>(P, 2048));
     nsplit = (int)std::max<int64_t>(1, P / chunk);
   } else {
     // >= 512 rows per split CTA and at most 8 splits (partials stay a few
-    // percent of the Grammian's reads), or the fixed HZG_SPLIT_ROWS; a
+    // percent of the Grammian's reads), or the configured split_rows; a
     // power-of-two count, chunk a multiple of 64 rows.  Depends on m only,
     // never on the GPU count.
     nsplit = kSplitRows > 0 ? (int)pow2c((m + kSplitRows - 1) / kSplitRows)
@@ -214,7 +226,8 @@ void gram_split(int64_t m, bool exact, int& nsplit, int64_t& chunk) {
 }
 
 struct Layout {
-  size_t colpair, itable, part, zt, ident, zt2, ident2, counts, ctr, status, qr, qrlock, fin, sig, phase, comp, pg, total;
+  size_t colpair, itable, part, zt, ident, zt2, ident2, counts, ctr, status, qr, qrlock, fin, sig, phase, comp, pg, red,
+      total;
 };
 
 Layout layout(const hzg_ctx* c) {
@@ -252,6 +265,7 @@ Layout layout(const hzg_ctx* c) {
   L.comp = take(cs);
   L.pg = take((c->pg_chains_host.size() + c->pg_links_host.size() + c->pg_exc_host.size() +
                c->all_pairs_host.size()) * 4);
+  L.red = take(8 * 8);
   L.total = off;
   return L;
 }
@@ -427,6 +441,23 @@ void build_postgram_tables(hzg_ctx* c) {
   for (int i = 0; i < np; ++i) c->all_pairs_host[i] = i;
 }
 
+// Cross-rank reduction vector of one rank sweep (hzg_dist_sweep): the
+// integer counters, and the status bits as per-kind indicators (NCCL has no
+// bitwise-or reduction; a sum of indicators is exact and order-free)
+__global__ void k_red_pack(const int64_t* ctr, int64_t* red) {
+  if (threadIdx.x != 0) return;
+  const int64_t st = ctr[2];
+  red[0] = ctr[0];
+  red[1] = ctr[1];
+  red[2] = st != 0;
+  red[3] = (st & ST_NOT_PD) != 0;
+  red[4] = (st & (ST_RANK | ST_QR_RANK)) != 0;
+}
+
+__global__ void k_red_status(const int32_t* status, int64_t* red) {
+  if (threadIdx.x == 0) red[5] = status[0] != 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -478,7 +509,7 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   std::vector<int32_t> inner;
   c->isteps = gen_table(cfg->inner_mm != 0, c->tw, inner);
   c->itable_host.assign(inner.begin(), inner.begin() + (size_t)c->isteps * c->tw);
-  for (int mat = 0; mat < 2; ++mat) gram_split(mat == 0 ? mF : mG, !c->use_dmma, c->gw.nsplit[mat], c->gw.chunk[mat]);
+  for (int mat = 0; mat < 2; ++mat) gram_split(mat == 0 ? mF : mG, !c->use_dmma, cfg->split_rows, c->gw.nsplit[mat], c->gw.chunk[mat]);
   if (c->comp) {  // the compensated Grammian is one sequential form over the full height
     c->gw.nsplit[0] = c->gw.nsplit[1] = 1;
     c->gw.chunk[0] = mF;
@@ -487,7 +518,7 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   c->gw.smax = std::max(c->gw.nsplit[0], c->gw.nsplit[1]);
   // fused postmultiply + Grammian: DMMA mode, real, w = 16, the ME circle
   // schedule of a single rank, splits of at most 256 rows.  Opt-in
-  // (HZG_FUSED=1 with HZG_SPLIT_ROWS=256): bitwise equal to the separate
+  // (HZG_FUSED=1 with SolverConfig(split_rows=256)): bitwise equal to the separate
   // kernels, but measured slower on B200 so far (profiles/r01_fused.txt)
   {
     const char* env = std::getenv("HZG_FUSED");
@@ -522,6 +553,13 @@ int hzg_set_schedule(hzg_ctx* c, const int32_t* colpairs, int32_t osteps, int32_
   return HZG_OK;
 }
 
+int hzg_set_z_rows(hzg_ctx* c, int64_t zrows) {
+  if (!c || zrows < c->n) return HZG_INVALID;
+  if (c->bound) return fail(c, HZG_INVALID, "hzg_set_z_rows must precede hzg_bind");
+  c->zrows = zrows;
+  return HZG_OK;
+}
+
 int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double* Zr, double* Zi, void* workspace,
              void* stream) {
   if (!c || !Fr || !Gr || !Zr || !workspace) return HZG_INVALID;
@@ -530,7 +568,8 @@ int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double*
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
   c->F = Plane{Fr, c->cplx ? Fi : nullptr, c->mF, c->mF};
   c->G = Plane{Gr, c->cplx ? Gi : nullptr, c->mG, c->mG};
-  c->Z = Plane{Zr, c->cplx ? Zi : nullptr, c->n, c->n};
+  const int64_t zr = c->zrows > 0 ? c->zrows : c->n;
+  c->Z = Plane{Zr, c->cplx ? Zi : nullptr, zr, zr};
   c->stream = (cudaStream_t)stream;
   Layout L = layout(c);
   c->ws = (unsigned char*)workspace;
@@ -550,6 +589,7 @@ int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double*
   c->d_sig = (double*)(c->ws + L.sig);
   c->d_phase = (long long*)(c->ws + L.phase);
   c->d_comp = c->comp ? (double*)(c->ws + L.comp) : nullptr;
+  c->d_red = (int64_t*)(c->ws + L.red);
   c->io.phase = nullptr;
   if ((e = cudaMemcpyAsync(c->d_colpair, c->colpair_host.data(), c->colpair_host.size() * 4,
                            cudaMemcpyHostToDevice, c->stream)) != cudaSuccess)
@@ -597,7 +637,7 @@ int hzg_bind(hzg_ctx* c, double* Fr, double* Fi, double* Gr, double* Gi, double*
 int hzg_init_fgz(hzg_ctx* c) {
   if (!c || !c->bound) return HZG_INVALID;
   cudaError_t e;
-  const size_t zb = (size_t)c->n * c->n * 8;
+  const size_t zb = (size_t)c->Z.rows * c->n * 8;
   cudaMemsetAsync(c->Z.re, 0, zb, c->stream);
   if (c->Z.im) cudaMemsetAsync(c->Z.im, 0, zb, c->stream);
   cudaMemsetAsync(c->d_status, 0, 16, c->stream);
@@ -984,6 +1024,16 @@ int hzg_finalize(hzg_ctx* c, int64_t n0, int64_t mF0, int64_t mG0, int32_t sort,
   double* sF = c->d_sig;
   double* sG = sF + c->n;
   double* s = sG + c->n;
+  // a Z rescale queued after the last sweep's counters (the step-wise
+  // drivers: hzg_collect, then hzg_rescale_z) has not been checked yet
+  if ((e = cudaMemcpyAsync(c->h_ctr, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "status copy");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "final rescale");
+  {
+    int32_t pending = 0;
+    std::memcpy(&pending, c->h_ctr, 4);
+    if (pending) return fail(c, HZG_RANK, "zero pencil column between sweeps");
+  }
   cudaMemsetAsync(c->d_status, 0, 16, c->stream);
   int rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 1, sF, sG, s, nullptr, c->d_status,
                           c->comp ? c->d_comp : nullptr, c->cstride, c->stream);
@@ -1164,7 +1214,7 @@ int hzg_op_grammian(int64_t m, int32_t w, int32_t cplx, int32_t comp, const doub
   GramWS gw{};
   int nsplit = 1;
   int64_t chunk = m;
-  if (!comp) gram_split(m, true, nsplit, chunk);
+  if (!comp) gram_split(m, true, 0, nsplit, chunk);
   gw.nsplit[0] = gw.nsplit[1] = nsplit;
   gw.chunk[0] = gw.chunk[1] = chunk;
   gw.smax = nsplit;
@@ -1264,8 +1314,252 @@ int hzg_test_fastmath(int64_t n, uint64_t seed, int64_t* counts4) {
 
 const char* hzg_last_error(const hzg_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+
+// ---------------------------------------------------------------------------
+// multi-GPU data plane: NCCL inside libhzg
+// ---------------------------------------------------------------------------
+
+int hzg_comm_unique_id(void* id_out) {
+  if (!id_out) return HZG_INVALID;
+  std::string err;
+  const hzg::nccl::Api* nc = hzg::nccl::load(err);
+  if (!nc) return HZG_CUDA;
+  ncclUniqueId id;
+  if (nc->GetUniqueId(&id) != ncclSuccess) return HZG_CUDA;
+  std::memcpy(id_out, &id, sizeof(id));
+  return HZG_OK;
+}
+
+size_t hzg_comm_unique_id_bytes(void) { return sizeof(ncclUniqueId); }
+
+static int nccl_fail(hzg_ctx* c, ncclResult_t r, const char* where) {
+  c->err = std::string(where) + ": " + (c->nc ? c->nc->GetErrorString(r) : "nccl");
+  return HZG_CUDA;
+}
+
+int hzg_comm_attach(hzg_ctx* c, int32_t nranks, int32_t rank, const void* unique_id) {
+  if (!c || !unique_id || nranks < 1 || rank < 0 || rank >= nranks) return HZG_INVALID;
+  if (c->comm) return fail(c, HZG_INVALID, "communicator already attached");
+  std::string err;
+  c->nc = hzg::nccl::load(err);
+  if (!c->nc) return fail(c, HZG_CUDA, err.c_str());
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ncclResult_t r = c->nc->CommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    c->comm = nullptr;
+    return nccl_fail(c, r, "ncclCommInitRank");
+  }
+  c->nranks = nranks;
+  c->rank = rank;
+  return HZG_OK;
+}
+
+int hzg_comm_set_moves(hzg_ctx* c, const int32_t* moves, const int32_t* offsets, int32_t osteps) {
+  if (!c || !offsets || osteps != c->osteps) return HZG_INVALID;
+  if (offsets[0] != 0) return HZG_INVALID;
+  for (int k = 0; k < osteps; ++k)
+    if (offsets[k + 1] < offsets[k]) return HZG_INVALID;
+  const int32_t total = offsets[osteps];
+  if (total > 0 && !moves) return HZG_INVALID;
+  c->moves.clear();
+  c->move_off.assign(1, 0);
+  for (int k = 0; k < osteps; ++k) {
+    for (int32_t q = offsets[k]; q < offsets[k + 1]; ++q) {
+      const int32_t b = moves[3 * q], src = moves[3 * q + 1], dst = moves[3 * q + 2];
+      if (b < 0 || b >= c->nblk || src < 0 || src >= c->nranks || dst < 0 || dst >= c->nranks)
+        return fail(c, HZG_INVALID, "block move out of range");
+      if (src != c->rank && dst != c->rank) continue;  // not this rank's business
+      c->moves.insert(c->moves.end(), {b, src, dst});
+    }
+    c->move_off.push_back((int32_t)(c->moves.size() / 3));
+  }
+  if (c->dgexec) {
+    cudaGraphExecDestroy(c->dgexec);
+    c->dgexec = nullptr;
+  }
+  if (c->dgraph) {
+    cudaGraphDestroy(c->dgraph);
+    c->dgraph = nullptr;
+  }
+  return HZG_OK;
+}
+
+// Grouped send / recv of whole block columns of F, G, Z (each block is one
+// contiguous w * rows range of every plane).  A block whose source and
+// destination are both this rank is sent to itself.
+static int emit_exchange(hzg_ctx* c, const int32_t* mv, int count, cudaStream_t s) {
+  if (count <= 0) return HZG_OK;
+  const hzg::nccl::Api* nc = c->nc;
+  const Plane* pl[3] = {&c->F, &c->G, &c->Z};
+  ncclResult_t r = nc->GroupStart();
+  if (r != ncclSuccess) return nccl_fail(c, r, "ncclGroupStart");
+  for (int q = 0; q < count && r == ncclSuccess; ++q) {
+    const int32_t b = mv[3 * q], src = mv[3 * q + 1], dst = mv[3 * q + 2];
+    for (int m = 0; m < 3 && r == ncclSuccess; ++m) {
+      const size_t cnt = (size_t)c->w * pl[m]->rows;
+      for (int part = 0; part < (c->cplx ? 2 : 1) && r == ncclSuccess; ++part) {
+        double* base = (part ? pl[m]->im : pl[m]->re) + (size_t)b * c->w * pl[m]->ld;
+        if (src == c->rank) r = nc->Send(base, cnt, ncclFloat64, dst, c->comm, s);
+        if (r == ncclSuccess && dst == c->rank) r = nc->Recv(base, cnt, ncclFloat64, src, c->comm, s);
+      }
+    }
+  }
+  ncclResult_t r2 = nc->GroupEnd();
+  if (r != ncclSuccess) return nccl_fail(c, r, "ncclSend/ncclRecv");
+  if (r2 != ncclSuccess) return nccl_fail(c, r2, "ncclGroupEnd");
+  return HZG_OK;
+}
+
+int hzg_comm_exchange(hzg_ctx* c, const int32_t* moves, int32_t count) {
+  if (!c || !c->bound || !c->comm || count < 0 || (count > 0 && !moves)) return HZG_INVALID;
+  std::vector<int32_t> mine;
+  for (int q = 0; q < count; ++q) {
+    const int32_t b = moves[3 * q], src = moves[3 * q + 1], dst = moves[3 * q + 2];
+    if (b < 0 || b >= c->nblk || src < 0 || src >= c->nranks || dst < 0 || dst >= c->nranks)
+      return fail(c, HZG_INVALID, "block move out of range");
+    if (src == c->rank || dst == c->rank) mine.insert(mine.end(), {b, src, dst});
+  }
+  int rc = emit_exchange(c, mine.data(), (int)(mine.size() / 3), c->stream);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  return e == cudaSuccess ? HZG_OK : cuda_fail(c, e, "exchange");
+}
+
+// One rank's outer sweep as ONE CUDA graph: its slot range of every step as
+// position groups on the group streams (wavefront, as in build_graph), the
+// block exchange after every step on the exchange stream (grouped NCCL
+// send / recv; the end groups of step k+1 wait for it, it waits for the end
+// groups of step k -- the blocks that change owner sit at the ends of the
+// rank's range), then the counter fold, an all-reduce of the counters and
+// status indicators, the Z rescale gated on the GLOBAL big count, and an
+// all-reduce of its status.  No host synchronisation inside the sweep.
+static int build_dist_graph(hzg_ctx* c) {
+  cudaError_t e;
+  int G = std::max(1, std::min(8, c->npairs / 16));
+  if (const char* env = std::getenv("HZG_GROUPS")) G = std::max(1, std::min(c->npairs, std::atoi(env)));
+  c->dgroups = G;
+  if (int rc = stream_pool(c, c->gstreams, G, true)) return rc;
+  if (!c->xstream) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if ((e = cudaStreamCreateWithPriority(&c->xstream, cudaStreamNonBlocking, greatest)) != cudaSuccess)
+      return cuda_fail(c, e, "cudaStreamCreate");
+  }
+  const size_t nev = 3 + 3 * (size_t)G;
+  while (c->devents.size() < nev) {
+    cudaEvent_t ev;
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(c, e, "cudaEventCreate");
+    c->devents.push_back(ev);
+  }
+  cudaEvent_t fork = c->devents[0], xev = c->devents[1], xjoin = c->devents[2];
+  cudaEvent_t* join = &c->devents[3];
+  cudaEvent_t* sev = &c->devents[3 + G];  // [2][G]
+  if ((e = cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+    return cuda_fail(c, e, "begin capture");
+  int rc = HZG_OK;
+  cudaEventRecord(fork, c->cap);
+  for (int g = 0; g < G; ++g) cudaStreamWaitEvent(c->gstreams[g], fork, 0);
+  cudaStreamWaitEvent(c->xstream, fork, 0);
+  for (int st = 0; st < c->osteps && rc == HZG_OK; ++st) {
+    for (int g = 0; g < G && rc == HZG_OK; ++g) {
+      cudaStream_t s = c->gstreams[g];
+      if (st > 0) {
+        if (g > 0) cudaStreamWaitEvent(s, sev[((st - 1) & 1) * G + g - 1], 0);
+        if (g + 1 < G) cudaStreamWaitEvent(s, sev[((st - 1) & 1) * G + g + 1], 0);
+        if (g == 0 || g == G - 1) cudaStreamWaitEvent(s, xev, 0);
+      }
+      const int p0 = group_cut(c->npairs, G, g), p1 = group_cut(c->npairs, G, g + 1);
+      rc = launch_step(c, st, s, nullptr, p0, p1 - p0);
+      cudaEventRecord(sev[(st & 1) * G + g], s);
+    }
+    if (rc) break;
+    const int nm = c->move_off.empty() ? 0 : c->move_off[st + 1] - c->move_off[st];
+    if (nm > 0) {
+      cudaStreamWaitEvent(c->xstream, sev[(st & 1) * G + 0], 0);
+      cudaStreamWaitEvent(c->xstream, sev[(st & 1) * G + G - 1], 0);
+      rc = emit_exchange(c, c->moves.data() + 3 * (size_t)c->move_off[st], nm, c->xstream);
+    }
+    cudaEventRecord(xev, c->xstream);
+  }
+  for (int g = 0; g < G; ++g) {
+    cudaEventRecord(join[g], c->gstreams[g]);
+    cudaStreamWaitEvent(c->cap, join[g], 0);
+  }
+  cudaEventRecord(xjoin, c->xstream);
+  cudaStreamWaitEvent(c->cap, xjoin, 0);
+  if (rc == HZG_OK) rc = launch_counters(c->io.counts, (int64_t)c->osteps * c->npairs, c->d_ctr, c->cap);
+  if (rc == HZG_OK) {
+    k_red_pack<<<1, 32, 0, c->cap>>>(c->d_ctr, c->d_red);
+    ncclResult_t r = c->nc->AllReduce(c->d_red, c->d_red, 5, ncclInt64, ncclSum, c->comm, c->cap);
+    if (r != ncclSuccess) rc = nccl_fail(c, r, "ncclAllReduce(counters)");
+  }
+  if (rc == HZG_OK)
+    rc = launch_rescale(c->F, c->G, c->Z, c->n, c->cplx, 0, nullptr, nullptr, nullptr, c->d_red, c->d_status,
+                        c->comp ? c->d_comp : nullptr, c->cstride, c->cap);
+  if (rc == HZG_OK) {
+    k_red_status<<<1, 32, 0, c->cap>>>(c->d_status, c->d_red);
+    ncclResult_t r = c->nc->AllReduce(c->d_red + 5, c->d_red + 5, 1, ncclInt64, ncclSum, c->comm, c->cap);
+    if (r != ncclSuccess) rc = nccl_fail(c, r, "ncclAllReduce(status)");
+  }
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(c->cap, &g);
+  if (rc != HZG_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc == HZG_CUDA && !c->err.empty() ? rc : fail(c, rc, "launch during capture");
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "end capture");
+  c->dgraph = g;
+  if ((e = cudaGraphInstantiate(&c->dgexec, g, cudaGraphInstantiateFlagUseNodePriority)) != cudaSuccess)
+    return cuda_fail(c, e, "graph instantiate");
+  return HZG_OK;
+}
+
+int hzg_dist_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
+  if (!c || !c->bound || !c->comm) return HZG_INVALID;
+  if ((int)c->move_off.size() != c->osteps + 1) return fail(c, HZG_INVALID, "hzg_comm_set_moves first");
+  cudaError_t e;
+  if (!c->dgexec) {
+    if (int rc = build_dist_graph(c)) return rc;
+  }
+  if ((e = cudaGraphLaunch(c->dgexec, c->stream)) != cudaSuccess) return cuda_fail(c, e, "graph launch");
+  if ((e = cudaMemcpyAsync(c->h_ctr, c->d_red, 6 * 8, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
+    return cuda_fail(c, e, "counter copy");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "dist sweep");
+  ncclResult_t async = ncclSuccess;
+  c->nc->CommGetAsyncError(c->comm, &async);
+  if (async != ncclSuccess) return nccl_fail(c, async, "NCCL async error");
+  if (total) *total = c->h_ctr[0];
+  if (big) *big = c->h_ctr[1];
+  // every rank holds the same reduced indicators, so every rank raises the
+  // same error (no rank leaves the job while the others wait in NCCL)
+  if (c->h_ctr[3]) return fail(c, HZG_NOT_PD, "indefinite block Grammian; enable the QR fallback");
+  if (c->h_ctr[4]) return fail(c, HZG_RANK, "rank-deficient block pair in the inner solve");
+  if (c->h_ctr[5]) return fail(c, HZG_RANK, "zero pencil column between sweeps");
+  return HZG_OK;
+}
+
+int hzg_comm_detach(hzg_ctx* c) {
+  if (!c) return HZG_INVALID;
+  if (c->dgexec) cudaGraphExecDestroy(c->dgexec);
+  if (c->dgraph) cudaGraphDestroy(c->dgraph);
+  c->dgexec = nullptr;
+  c->dgraph = nullptr;
+  if (c->comm && c->nc) c->nc->CommDestroy(c->comm);
+  c->comm = nullptr;
+  c->nranks = 1;
+  c->rank = 0;
+  return HZG_OK;
+}
+
 void hzg_destroy(hzg_ctx* c) {
   if (!c) return;
+  hzg_comm_detach(c);
+  for (auto& e : c->devents) cudaEventDestroy(e);
+  if (c->xstream) cudaStreamDestroy(c->xstream);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->cap) cudaStreamDestroy(c->cap);

@@ -416,12 +416,16 @@ struct GatherParams {
   const double *sF, *sG, *s;
   double *sFo, *sGo, *so;
   const int32_t* rank;
+  int64_t n0;  // output columns: a rank >= n0 (unborder mismatch) writes nothing
 };
 
 __global__ void k_gather(GatherParams P) {
   const int64_t j = blockIdx.x;
   const int32_t r = P.rank[j];
-  if (r < 0) return;
+  // r >= n0 only when unbordering kept more than n0 columns; k_keep_count
+  // has flagged ST_RANK and the host raises RankError after finalize, so
+  // the gather must not write past the n0-column outputs meanwhile
+  if (r < 0 || r >= P.n0) return;
   for (int m = 0; m < 3; ++m) {
     const Plane& a = P.in[m];
     const Plane& b = P.out[m];
@@ -592,7 +596,7 @@ int launch_finalize(const Plane& U, const Plane& V, const Plane& Z, int64_t n, i
   k_keep<<<(unsigned)((n + tb - 1) / tb), tb, 0, s>>>(Z, n, n0, keep);
   k_keep_count<<<1, 1024, 0, s>>>(keep, n, n0, status);
   k_rank<<<(unsigned)((n + tb - 1) / tb), tb, tb * (sizeof(double) + sizeof(int32_t)), s>>>(sig, keep, n, sort, rank);
-  GatherParams g{{U, V, Z}, {Uo, Vo, Zo}, sigF, sigG, sig, sFo, sGo, so, rank};
+  GatherParams g{{U, V, Z}, {Uo, Vo, Zo}, sigF, sigG, sig, sFo, sGo, so, rank, n0};
   k_gather<<<(unsigned)n, 256, 0, s>>>(g);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }

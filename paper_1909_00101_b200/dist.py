@@ -17,9 +17,14 @@ geometry, same per-pair data), so the result is bitwise independent of the
 number of ranks; the per-sweep counters are integers summed with an
 all-reduce.
 
-Transports:
-  * DistTransport -- torch.distributed P2P (NCCL on GPUs; gloo for the CPU
-    tests of the routing);
+Data planes:
+  * NCCL jobs (one process per GPU): libhzg owns the exchange -- grouped
+    ncclSend / ncclRecv of the crossing blocks after every step and the
+    counter all-reduce, captured with the rank's steps into ONE CUDA graph
+    per sweep (hzg_dist_sweep); torch.distributed only broadcasts the
+    ncclUniqueId;
+  * DistTransport -- torch.distributed P2P over gloo (the CPU tests of the
+    routing, and several ranks sharing one GPU in the GPU tests);
   * LocalTransport -- R virtual ranks in one process (one device), block
     exchange by device copies; used by solve(workers=R) and the tests.
 """
@@ -29,6 +34,7 @@ import os
 
 import numpy as np
 
+from . import _native
 from .strategies import circle_positions, slot_ranges, weighted_slot_ranges
 
 
@@ -286,13 +292,17 @@ def sweep_ranks(devs, sched, transport, allreduce=None, wave=None):
             transport.exchange(sched.moves(k))
     else:
         _sweep_wavefront(devs, sched, transport, wave)
-    t = b = 0
+    t = b = code = 0
     for d in devs:
-        tt, bb = d.collect()
+        tt, bb, cc = d.collect_status()
         t += tt
         b += bb
+        code = max(code, cc)
     if allreduce is not None:
-        t, b = allreduce(t, b)
+        # every rank learns the worst status before anyone raises, so no
+        # rank leaves the job while the others wait in the next exchange
+        t, b, code = allreduce(t, b, code)
+    _native.check(code, None, "block pair of this sweep (status agreed over all ranks)")
     if b != 0:
         for d in devs:
             d.rescale_z()
@@ -330,6 +340,7 @@ class PartitionedGsvd:
         self.sched = BlockSchedule(self.nblk, self.nranks)
         epsn = epsn_of(cfg, n)
         self.comm = comm
+        self.nccl = False
         if comm is None:
             plist = [planes] + [{k: (v.clone() if v is not None else None) for k, v in planes.items()}
                                 for _ in range(self.nranks - 1)]
@@ -350,23 +361,34 @@ class PartitionedGsvd:
             zgroup = _z_group(dist, world) if wavefront and split_z_default() else None
             self.transport = DistTransport(dict(planes, Zr=dev.Zr, Zi=dev.Zi), w, self.rank, zgroup=zgroup)
 
-            cdev = "cpu" if dist.get_backend() == "gloo" else dev.device
-
-            def allreduce(t, b):
-                x = torch.tensor([t, b], dtype=torch.int64, device=cdev)
-                dist.all_reduce(x)
-                return int(x[0]), int(x[1])
-
-            self.allreduce = allreduce
+            self.allreduce = counter_allreduce("cpu" if dist.get_backend() == "gloo" else dev.device)
+            if dist.get_backend() == "nccl" and os.environ.get("HZG_TORCH_P2P", "0") in ("", "0"):
+                # the data plane lives in libhzg: NCCL send / recv of the
+                # crossing blocks and the counter all-reduce inside one
+                # captured CUDA graph per sweep; torch.distributed only
+                # carries the ncclUniqueId
+                uid = [None]
+                if self.rank == 0:
+                    uid[0] = unique_id()
+                dist.broadcast_object_list(uid, src=0)
+                dev.comm_attach(world, self.rank, uid[0])
+                dev.comm_set_moves([self.sched.moves(k) for k in range(self.sched.steps)])
+                self.nccl = True
         ranks = range(self.nranks) if comm is None else [self.rank]
         self.wave = None
-        if wavefront and torch.cuda.is_available():
+        if wavefront and torch.cuda.is_available() and not self.nccl:
             self.wave = Wavefront(self.devs, [self.sched.ranges[r][1] - self.sched.ranges[r][0] for r in ranks],
                                   split_z=split_z_default())
         self.sweeps = self.total = self.big = 0
         self.converged = False
 
     def run(self):
+        if self.nccl:
+            self.init()
+            for _ in range(self.cfg.max_outer_sweeps):
+                if self.sweep()[1] == 0:
+                    break
+            return self
         self.sweeps, self.total, self.big, self.converged = run_ranks(self.devs, self.sched, self.transport, self.cfg,
                                                                       self.allreduce, self.wave)
         return self
@@ -379,7 +401,10 @@ class PartitionedGsvd:
 
     def sweep(self):
         """One outer sweep (after init()); returns (total, big)."""
-        t, b = sweep_ranks(self.devs, self.sched, self.transport, self.allreduce, self.wave)
+        if self.nccl:
+            t, b = self.devs[0].dist_sweep()
+        else:
+            t, b = sweep_ranks(self.devs, self.sched, self.transport, self.allreduce, self.wave)
         self.sweeps += 1
         self.total += t
         self.big += b
@@ -387,7 +412,10 @@ class PartitionedGsvd:
         return t, b
 
     def finalize(self, n0=None, mF0=None, mG0=None, sort=True):
-        self.transport.exchange(gather_blocks(self.sched))
+        if self.nccl:
+            self.devs[0].comm_exchange(gather_blocks(self.sched))
+        else:
+            self.transport.exchange(gather_blocks(self.sched))
         if self.rank != 0:
             return None
         root = self.devs[0]
@@ -395,6 +423,14 @@ class PartitionedGsvd:
         return root.finalize(n0, mF0, mG0, sort=sort)
 
     def launch_counts(self):
+        if self.nccl:
+            # hzg_dist_sweep: 3 kernels per position group and step, the
+            # counter fold, 2 status packs and the gated rescale per sweep
+            # (NCCL's own kernels not counted)
+            G = max(1, min(8, (self.sched.ranges[self.rank][1] - self.sched.ranges[self.rank][0]) // 16))
+            if os.environ.get("HZG_GROUPS"):
+                G = max(1, int(os.environ["HZG_GROUPS"]))
+            return self.sched.steps * 3 * G + 4, 6
         # step-wise driving: 3 kernels per step (per position group with the
         # wavefront), plus the counter fold and the Z rescale per sweep, per
         # rank driven by this process
@@ -408,6 +444,32 @@ class PartitionedGsvd:
     def close(self):
         for d in self.devs:
             d.close()
+
+
+def counter_allreduce(device):
+    """(total, big, status code) summed / maxed over the torch.distributed
+    ranks: every rank sees the same status, so all raise the same error
+    (HZG codes order by severity: OK 0 < RANK 1 < NOT_PD 2)."""
+    import torch
+    import torch.distributed as dist
+
+    def allreduce(t, b, code):
+        x = torch.tensor([t, b], dtype=torch.int64, device=device)
+        dist.all_reduce(x)
+        c = torch.tensor([code], dtype=torch.int64, device=device)
+        dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        return int(x[0]), int(x[1]), int(c[0])
+
+    return allreduce
+
+
+def unique_id():
+    """A new ncclUniqueId (bytes) from libhzg's NCCL binding."""
+    import ctypes
+    L = _native.load()
+    buf = ctypes.create_string_buffer(int(L.hzg_comm_unique_id_bytes()))
+    _native.check(L.hzg_comm_unique_id(buf), None, "ncclGetUniqueId")
+    return buf.raw
 
 
 def epsn_of(cfg, n):

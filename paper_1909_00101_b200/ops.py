@@ -5,8 +5,7 @@ preprocess_tall keep the reference's signatures and results
 (pkg/src/hzgsvd/blocked.py:328-428)
 and run the same reference-order kernels the solver uses (bitwise the
 reference), through the C ABI (include/hzg.h, hzg_op_*).  run_distributed
-(distsim.py:147) keeps its signature and runs the block-partitioned
-multi-rank schedule (dist.py) on the bordered pair.
+(distsim.py:147) is the reference's stripe-distributed scheme (stripes.py).
 """
 
 import ctypes
@@ -194,28 +193,7 @@ def rescale_z(F, G, Z, final=False, compensated=False):
 
 
 def run_distributed(p, cfg=None, s=2, s_inner=1, pool=1):
-    """Solve a bordered pair with s ranks (distsim.py:147 signature).
-
-    The B200 build distributes column blocks over ranks with the
-    block-partitioned schedule (dist.py); the result is bitwise that of a
-    single rank, i.e. of gsvd_blocked (columns in their original order).
-    ``s_inner`` and ``pool`` are accepted for signature compatibility."""
-    from .config import SolverConfig
-    from .dist import PartitionedGsvd
-    from .solver import _result_from_device, upload_bordered
-
-    cfg = cfg or SolverConfig()
-    if s < 1:
-        raise ValueError("need at least one worker")
-    w = cfg.block_width
-    if p.n % (2 * w * s) != 0:
-        raise ValueError("n=%d not divisible for %d workers at block width %d" % (p.n, s, w))
-    planes, n, mF, mG = upload_bordered(p.F, p.G, w)
-    job = PartitionedGsvd(planes, cfg, s)
-    try:
-        job.run()
-        out = job.finalize(n, p.F.rows, p.G.rows, sort=False)
-        r = _result_from_device(job.devs[0], out, p.is_complex, workers=s)
-        return r
-    finally:
-        job.close()
+    """Stripe-distributed solve of a bordered pair with s workers, the
+    reference's scheme and results (distsim.py:147-259; stripes.py)."""
+    from .stripes import run_distributed as _run
+    return _run(p, cfg, s, s_inner, pool)

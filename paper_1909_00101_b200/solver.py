@@ -42,10 +42,13 @@ class DeviceGsvd:
     planes: dict with keys Fr, Fi, Gr, Gi (torch float64 tensors of shape
     (n, m) -- column-major planes; imaginary ones None for real problems)
     already bordered to multiples of 2w.  Z planes and the workspace are
-    allocated here.
+    allocated here unless ``Z`` = (Zr, Zi) tensors of shape (n, zrows) are
+    given; ``zrows`` (default n) is the height of Z -- a stripe slab of
+    the reference's distributed scheme keeps the n global rows of Z for its
+    2W columns (stripes.py).
     """
 
-    def __init__(self, planes, cfg, device=None, epsn=None, schedule=None):
+    def __init__(self, planes, cfg, device=None, epsn=None, schedule=None, zrows=None, Z=None):
         torch = _torch()
         self.cfg = cfg
         self.torch = torch
@@ -67,9 +70,17 @@ class DeviceGsvd:
             sched = np.ascontiguousarray(schedule, dtype=np.int32)
             _native.check(lib.hzg_set_schedule(ctx, sched.ctypes.data_as(ctypes.c_void_p), sched.shape[0],
                                                sched.shape[1]), ctx, "hzg_set_schedule")
+        zrows = self.n if zrows is None else int(zrows)
+        if zrows != self.n:
+            _native.check(lib.hzg_set_z_rows(ctx, zrows), ctx, "hzg_set_z_rows")
         kw = dict(dtype=torch.float64, device=self.device)
-        self.Zr = torch.empty((self.n, self.n), **kw)
-        self.Zi = torch.empty((self.n, self.n), **kw) if self.cplx else None
+        if Z is not None:
+            self.Zr, self.Zi = Z
+            if tuple(self.Zr.shape) != (self.n, zrows) or not self.Zr.is_contiguous():
+                raise ValueError("Z planes must be contiguous (n, zrows) tensors")
+        else:
+            self.Zr = torch.empty((self.n, zrows), **kw)
+            self.Zi = torch.empty((self.n, zrows), **kw) if self.cplx else None
         self.ws = torch.empty(int(lib.hzg_workspace_bytes(ctx)), dtype=torch.uint8, device=self.device)
         self.stream = torch.cuda.current_stream(self.device)
         _native.check(lib.hzg_bind(ctx, _ptr(Fr), _ptr(planes.get("Fi")), _ptr(Gr), _ptr(planes.get("Gi")),
@@ -137,6 +148,49 @@ class DeviceGsvd:
         big = ctypes.c_int64(0)
         _native.check(self.lib.hzg_collect(self.ctx, ctypes.byref(tot), ctypes.byref(big)), self.ctx, "collect")
         return tot.value, big.value
+
+    def collect_status(self):
+        """collect() without raising: (total, big, status code), so a
+        multi-process caller can agree on the error before raising it."""
+        tot = ctypes.c_int64(0)
+        big = ctypes.c_int64(0)
+        rc = self.lib.hzg_collect(self.ctx, ctypes.byref(tot), ctypes.byref(big))
+        if rc not in (_native.HZG_OK, _native.HZG_RANK, _native.HZG_NOT_PD):
+            _native.check(rc, self.ctx, "collect")
+        return tot.value, big.value, rc
+
+    def dist_sweep(self):
+        """One outer sweep of this rank with the NCCL block exchange and
+        counter all-reduce inside the library (hzg_dist_sweep): global
+        (total, big)."""
+        tot = ctypes.c_int64(0)
+        big = ctypes.c_int64(0)
+        _native.check(self.lib.hzg_dist_sweep(self.ctx, ctypes.byref(tot), ctypes.byref(big)), self.ctx,
+                      "dist_sweep")
+        return tot.value, big.value
+
+    def comm_attach(self, nranks, rank, unique_id):
+        """Attach an NCCL communicator (hzg_comm_attach; collective)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), len(unique_id))
+        _native.check(self.lib.hzg_comm_attach(self.ctx, nranks, rank, buf), self.ctx, "comm_attach")
+
+    def comm_set_moves(self, moves_per_step):
+        """moves_per_step[k] = [(block, src, dst), ...] after step k."""
+        offs = np.zeros(len(moves_per_step) + 1, dtype=np.int32)
+        flat = []
+        for k, mv in enumerate(moves_per_step):
+            flat.extend(x for m in mv for x in m)
+            offs[k + 1] = offs[k] + len(mv)
+        arr = np.asarray(flat if flat else [0], dtype=np.int32)
+        _native.check(self.lib.hzg_comm_set_moves(self.ctx, arr.ctypes.data_as(ctypes.c_void_p),
+                                                  offs.ctypes.data_as(ctypes.c_void_p), len(moves_per_step)),
+                      self.ctx, "comm_set_moves")
+
+    def comm_exchange(self, moves):
+        """Immediate grouped NCCL exchange of whole blocks (block, src, dst)."""
+        arr = np.asarray([x for m in moves for x in m] or [0], dtype=np.int32)
+        _native.check(self.lib.hzg_comm_exchange(self.ctx, arr.ctypes.data_as(ctypes.c_void_p), len(moves)),
+                      self.ctx, "comm_exchange")
 
     def rescale_z(self):
         _native.check(self.lib.hzg_rescale_z(self.ctx), self.ctx, "rescale_z")
@@ -302,16 +356,30 @@ def gsvd_blocked(p, cfg=None, epsn=None):
     return r
 
 
-def solve(F, G, cfg=None, workers=1, worker_sweeps=1):
-    """Border, solve on the GPU, unborder, and sort a GSVD problem.
+def solve(F, G, cfg=None, workers=1, worker_sweeps=1, scheme="stripes", keep_context=True):
+    """Border, solve on the GPU, unborder, and sort a GSVD problem
+    (blocked.py:640-663).
 
-    F and G may be MatrixPlanePair values or numpy arrays.  With
-    ``workers`` > 1 the block-partitioned multi-rank schedule (dist.py)
-    runs with that many virtual ranks on the current device; a torchrun job
-    uses dist.solve_blocks(..., comm="dist") with one GPU per rank.  The
-    result does not depend on the rank count.  ``worker_sweeps`` is
-    accepted for signature compatibility (the block schedule has no inner
-    per-worker sweep cap).
+    F and G may be MatrixPlanePair values or numpy arrays.  ``workers`` > 1
+    selects a multi-worker schedule with ``scheme``:
+
+    * "stripes" (default, the reference's semantics): the stripe-distributed
+      scheme of distsim.py -- the pair is bordered to a multiple of
+      2w * workers, each outermost step runs up to ``worker_sweeps`` sweeps
+      on every worker's two-stripe slab, then the stripes move along the
+      communication mapping.  Results depend on ``workers`` exactly as the
+      reference's do (stripes.py);
+    * "blocks": the B200 block-partitioned schedule (dist.py) -- the
+      single-worker ME schedule with its block pairs split over ``workers``
+      ranks; bitwise the single-worker result for any rank count (the
+      multi-GPU production path; here the ranks are virtual ranks on the
+      current device, a torchrun job uses dist.solve_blocks).
+
+    ``keep_context`` (single worker): keep the device context (planes,
+    workspace, captured sweep graph: about 3.3 n^2 doubles plus the inputs)
+    for the next solve of the same shape and configuration, so the sweep
+    graph is captured once; False releases it before returning
+    (clear_cache() does the same at any time).
     """
     cfg = cfg or SolverConfig()
     if isinstance(F, np.ndarray):
@@ -320,19 +388,31 @@ def solve(F, G, cfg=None, workers=1, worker_sweeps=1):
         G = MatrixPlanePair.from_dense(G)
     if workers < 1:
         raise ValueError("need at least one worker")
+    if scheme not in ("stripes", "blocks"):
+        raise ValueError("scheme must be 'stripes' or 'blocks'")
     _torch()  # no device or no libhzg.so: fail loudly, also for the 1x1 closed form
     _native.load()
     if F.cols == 1:
         return gsvd_1x1(F, G)
-    if workers > 1:
+    if workers > 1 and scheme == "blocks":
         from .dist import solve_blocks
         return solve_blocks(F, G, cfg, workers)
     p = ProblemPair(F, G)
+    if workers > 1:
+        from .core import border_pair
+        from .stripes import run_distributed, sort_descending, unborder
+        w = cfg.block_width
+        pb = border_pair(p, 2 * w * workers, 2 * w)
+        return sort_descending(unborder(run_distributed(pb, cfg, workers, worker_sweeps), pb))
     with _cache_lock:
         dev = _cached_solver(p, cfg)
-        dev.run()
-        out = dev.finalize(p.n, p.F.rows, p.G.rows, sort=True)
-        return _result_from_device(dev, out, p.is_complex, workers)
+        try:
+            dev.run()
+            out = dev.finalize(p.n, p.F.rows, p.G.rows, sort=True)
+            return _result_from_device(dev, out, p.is_complex, workers)
+        finally:
+            if not keep_context:
+                clear_cache()
 
 
 # The last solve's device context (planes, workspace, captured sweep graph)
@@ -345,9 +425,13 @@ _cache = {"key": None, "dev": None}
 def _cached_solver(p, cfg):
     torch = _torch()
     w = cfg.block_width
-    # the HZG_* tuning variables shape the context too
+    # the HZG_* performance variables shape the context too (graph layout,
+    # stream use; none of them changes result bits), and so does the stream
+    # the context was bound to
     knobs = tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("HZG_")))
-    key = (torch.cuda.current_device(), p.n, p.F.rows, p.G.rows, p.is_complex, dataclasses.astuple(cfg), knobs)
+    stream = torch.cuda.current_stream().cuda_stream
+    key = (torch.cuda.current_device(), stream, p.n, p.F.rows, p.G.rows, p.is_complex,
+           dataclasses.astuple(cfg), knobs)
     if _cache["key"] == key:
         dev = _cache["dev"]
         upload_bordered(p.F, p.G, w, out=dev.planes)

@@ -37,7 +37,7 @@ def test_error_hierarchy():
     assert issubclass(hz.ProtocolError, hz.HzgsvdError)
 
 
-def test_plane_pair_validation_and_roundtrip(tmp_path):
+def test_plane_pair_validation():
     with pytest.raises(ValueError):
         hz.MatrixPlanePair(2, 2, np.zeros((2, 3)))
     with pytest.raises(ValueError):
@@ -45,13 +45,12 @@ def test_plane_pair_validation_and_roundtrip(tmp_path):
     with pytest.raises(ValueError):
         hz.ProblemPair(hz.MatrixPlanePair.from_dense(np.ones((2, 3))), hz.MatrixPlanePair.from_dense(np.ones((4, 3))))
     m = hz.MatrixPlanePair.from_dense(np.arange(6.0).reshape(3, 2) + 1j)
-    hz.write_matrix(m, str(tmp_path / "a.bin"))
-    r = hz.read_matrix(str(tmp_path / "a.bin"), str(tmp_path / "a.bin.hdr"))
-    assert np.array_equal(r.to_dense(), m.to_dense())
-    with open(tmp_path / "a.bin", "ab") as fh:
-        fh.write(b"x")
-    with pytest.raises(hz.FileFormatError):
-        hz.read_matrix(str(tmp_path / "a.bin"), str(tmp_path / "a.bin.hdr"))
+    assert m.is_complex and np.array_equal(m.to_dense(), np.arange(6.0).reshape(3, 2) + 1j)
+    c = m.copy()
+    c.re[0, 0] = 99.0
+    assert m.re[0, 0] == 0.0
+    flat = hz.MatrixPlanePair(2, 2, np.arange(4.0))
+    assert np.array_equal(flat.re, np.arange(4.0).reshape((2, 2), order="F"))
 
 
 @pytest.mark.parametrize("shape", [(5, 3, 2), (16, 16, 4), (70, 45, 8), (33, 20, 16)])
@@ -63,6 +62,11 @@ def test_border_pair_matches_oracle(shape):
     pad = (-n) % (2 * w)
     R, _ = O.border_one(A, None, pad, 2 * w)
     assert np.array_equal(b.F.re, R)
+    Ac = A + 1j * A[::-1]
+    pc = hz.ProblemPair(hz.MatrixPlanePair.from_dense(Ac), hz.MatrixPlanePair.from_dense(Ac))
+    bc = hz.border_pair(pc, 2 * w, 2 * w)
+    Rr, Ri = O.border_one(Ac.real.copy(), Ac.imag.copy(), pad, 2 * w)
+    assert np.array_equal(bc.F.re, Rr) and np.array_equal(bc.G.im, Ri)
     assert (b.original_n, b.original_mF) == (n, m)
     assert hz.core.bordered_shape(n, m, 2 * w, 2 * w) == (pad, R.shape[0])
 
@@ -134,3 +138,17 @@ def test_no_cpu_fallback_without_device():
         pytest.skip("device present")
     with pytest.raises(hz.DeviceError):
         hz.solve(np.eye(4), np.eye(4), hz.SolverConfig(block_width=2))
+
+
+def test_product_package_never_uses_the_oracle():
+    """The oracle is test infrastructure: no module of the product package
+    may import, load or execute anything under oracle/ (DESIGN.md section 2)."""
+    import pathlib
+    pkg = pathlib.Path(hz.__file__).parent
+    offenders = []
+    for path in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.h")) + list(pkg.rglob("*.cuh")):
+        text = path.read_text()
+        for pat in ("import oracle", "from oracle", "hzg_oracle", "libhzg_oracle", "oracle/", "hzo_"):
+            if pat in text:
+                offenders.append("%s: %s" % (path.name, pat))
+    assert not offenders, offenders

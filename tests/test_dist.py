@@ -146,3 +146,58 @@ def test_weighted_schedule_covers_every_pair():
             for c0, c1 in cp[k]:
                 seen.add((c0 // w, c1 // w))
     assert len(seen) == nblk * (nblk - 1) // 2
+
+
+class _FakeDev:
+    """A rank whose inner solve reports `code` (0 ok, 1 RankError, 2 not PD)."""
+
+    def __init__(self, code):
+        self.code = code
+        self.rescaled = 0
+
+    def run_steps(self, k, count):
+        pass
+
+    def collect_status(self):
+        return 10, 3, self.code
+
+    def rescale_z(self):
+        self.rescaled += 1
+
+
+class _NoTransport:
+    def exchange(self, moves, keys=None):
+        pass
+
+
+def _status_worker(rank, world, port, codes, out):
+    from paper_1909_00101_b200 import NotPositiveDefiniteError, RankError
+    from paper_1909_00101_b200.dist import counter_allreduce, sweep_ranks
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sched = BlockSchedule(4 * world, world)
+    dev = _FakeDev(codes[rank])
+    try:
+        t, b = sweep_ranks([dev], sched, _NoTransport(), counter_allreduce("cpu"))
+        res = ("ok", t, b, dev.rescaled)
+    except NotPositiveDefiniteError:
+        res = ("notpd",)
+    except RankError:
+        res = ("rank",)
+    # every rank reaches this collective: nobody left the job early
+    dist.barrier()
+    torch.save(res, "%s.%d" % (out, rank))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("codes,expect", [((0, 0, 0), ("ok", 30, 9, 1)), ((0, 1, 0), ("rank",)),
+                                          ((2, 1, 0), ("notpd",))])
+def test_gloo_status_agreed_before_raising(tmp_path, codes, expect):
+    """A failing block pair on one rank raises the same error on EVERY rank
+    (the status is all-reduced with the counters) instead of leaving the
+    others waiting in the next exchange (dist.py)."""
+    out = str(tmp_path / "res")
+    mp.spawn(_status_worker, args=(3, _free_port(), codes, out), nprocs=3, join=True)
+    for r in range(3):
+        assert torch.load("%s.%d" % (out, r)) == expect

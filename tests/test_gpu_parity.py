@@ -8,6 +8,7 @@
   bitwise reproducible run to run.
 """
 
+import dataclasses
 import ctypes
 
 import numpy as np
@@ -363,12 +364,12 @@ def test_fused_postgram_bitwise_equals_unfused(name, monkeypatch):
         g = O.gaussian_stream(77, 2 * 1024 * 1024)
         F = g[: 1024 * 1024].reshape((1024, 1024), order="F")
         G = g[1024 * 1024:].reshape((1024, 1024), order="F")
-        cfg = hz.SolverConfig(block_width=16)
+        cfg = hz.SolverConfig(block_width=16, split_rows=256)
     else:
         c = load_case(name)
-        F, G, cfg = c["F"], c["G"], _cfg(c)
-    monkeypatch.setenv("HZG_FUSED", "1")  # the fused path needs splits of <= 256 rows
-    monkeypatch.setenv("HZG_SPLIT_ROWS", "256")
+        F, G = c["F"], c["G"]
+        cfg = dataclasses.replace(_cfg(c), split_rows=256)  # the fused path needs splits of <= 256 rows
+    monkeypatch.setenv("HZG_FUSED", "1")
 
     def launches():
         p = hz.MatrixPlanePair.from_dense(F)
