@@ -1034,3 +1034,63 @@ int hzo_num_threads(void) {
   return 1;
 #endif
 }
+
+/* Timed CPU sample for bench.py (not a reference function): prescale the
+ * bordered planes, then run the outer steps listed in `steps` (indices into
+ * the outer table, in that order) of sweep 1 with the reference's
+ * per-step task pool (blocked.py:519-530), timing only the steps.  Spread
+ * indices sample the whole sweep's pair sets instead of step 0 repeatedly.
+ * Returns the status; *seconds = wall time of the steps. */
+int hzo_sample_steps(int64_t mF, int64_t mG, int64_t n, int cplx, double* Fr, double* Fi, double* Gr, double* Gi,
+                     double* Zr, double* Zi, const hzo_cfg* cfg, int nthreads, const int32_t* steps, int nsteps,
+                     double* seconds) {
+  int w = cfg->block_width;
+  if (w < 1 || n % (2 * w) != 0) return HZO_INVALID;
+  plane_t F = {Fr, Fi, mF, n, mF}, G = {Gr, Gi, mG, n, mG}, Z = {Zr, Zi, n, n, n};
+  memset(Zr, 0, 8 * n * n); memset(Zi, 0, 8 * n * n);
+  int nblk = (int)(n / w), tw = 2 * w, half = nblk / 2;
+  int64_t mmax = mF > mG ? mF : mG;
+  if (n > mmax) mmax = n;
+  double* buf = (double*)malloc(8 * pow2(mmax));
+  double* z0 = (double*)malloc(8 * n);
+  for (int64_t j = 0; j < n; ++j) z0[j] = 1.0;
+  int st = HZO_OK;
+  if (cfg->prescale && prescale(F, G, z0, cplx, cfg->compensated, buf)) st = HZO_RANK;
+  for (int64_t j = 0; j < n; ++j) Zr[j + j * n] = z0[j];
+  double epsn = cfg->gate_eps * sqrt((double)n);
+  int32_t* outer = (int32_t*)malloc(sizeof(int32_t) * (int64_t)nblk * nblk);
+  int32_t* inner = (int32_t*)malloc(sizeof(int32_t) * (int64_t)tw * tw);
+  int osteps = hzo_gen_table(cfg->outer_mm, nblk, outer);
+  int isteps = hzo_gen_table(cfg->inner_mm, tw, inner);
+  if (nthreads < 1) nthreads = 1;
+  scratch_t* scr = (scratch_t*)malloc(sizeof(scratch_t) * nthreads);
+  for (int t = 0; t < nthreads; ++t) scratch_init(&scr[t], tw, mmax);
+  int* stv = (int*)malloc(sizeof(int) * half);
+  int64_t* tv = (int64_t*)malloc(sizeof(int64_t) * half);
+  int64_t* bv = (int64_t*)malloc(sizeof(int64_t) * half);
+  *seconds = 0.0;
+  for (int q = 0; q < nsteps && st == HZO_OK; ++q) {
+    int step = steps[q];
+    if (step < 0 || step >= osteps) { st = HZO_INVALID; break; }
+    const int32_t* row = outer + (int64_t)step * half * 2;
+    struct timespec ts0, ts1;
+    clock_gettime(CLOCK_MONOTONIC, &ts0);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+    for (int pr = 0; pr < half; ++pr) {
+      int tid = 0;
+#ifdef _OPENMP
+      tid = omp_get_thread_num();
+#endif
+      tv[pr] = 0; bv[pr] = 0;
+      stv[pr] = block_task(F, G, Z, cplx, row[2 * pr], row[2 * pr + 1], cfg, inner, isteps, epsn, &scr[tid],
+                           &tv[pr], &bv[pr]);
+    }
+    clock_gettime(CLOCK_MONOTONIC, &ts1);
+    *seconds += (double)(ts1.tv_sec - ts0.tv_sec) + 1e-9 * (double)(ts1.tv_nsec - ts0.tv_nsec);
+    for (int pr = 0; pr < half; ++pr)
+      if (stv[pr] != HZO_OK) { st = stv[pr]; break; }
+  }
+  for (int t = 0; t < nthreads; ++t) scratch_free(&scr[t]);
+  free(scr); free(stv); free(tv); free(bv); free(buf); free(z0); free(outer); free(inner);
+  return st;
+}

@@ -103,6 +103,31 @@ def cfg_from(cfg):
                     cfg.fallback_qr, cfg.shorten)
 
 
+def sample_steps(Fp, Gp, cfg, steps, threads=None):
+    """bench.py's CPU sample: prescale the bordered real planes, run the
+    listed outer steps of sweep 1 (reference task pool, all threads),
+    return the seconds spent in the steps (hzo_sample_steps)."""
+    L = lib()
+    P = ctypes.c_void_p
+    L.hzo_sample_steps.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, P, P, P, P, P, P,
+                                   ctypes.POINTER(_Cfg), ctypes.c_int, P, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_double)]
+    Fr = np.asfortranarray(Fp, dtype=np.float64).copy(order="F")
+    Gr = np.asfortranarray(Gp, dtype=np.float64).copy(order="F")
+    mF, n = Fr.shape
+    Fi = np.zeros_like(Fr, order="F")
+    Gi = np.zeros_like(Gr, order="F")
+    Zr = np.zeros((n, n), order="F")
+    Zi = np.zeros((n, n), order="F")
+    st = np.ascontiguousarray(steps, dtype=np.int32)
+    sec = ctypes.c_double(0.0)
+    rc = L.hzo_sample_steps(mF, Gr.shape[0], n, 0, _p(Fr), _p(Fi), _p(Gr), _p(Gi), _p(Zr), _p(Zi), ctypes.byref(cfg),
+                            threads or (os.cpu_count() or 1), _p(st), st.size, ctypes.byref(sec))
+    if rc:
+        raise OracleError(rc, "sample_steps")
+    return sec.value
+
+
 def gen_table(kind, n):
     """strategies.py:45-93 -> int32 (steps, n/2, 2)."""
     out = np.zeros((n, n // 2, 2), dtype=np.int32)

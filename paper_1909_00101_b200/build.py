@@ -17,6 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libhzg.so")
+PEAK_LIB = os.path.join(OUT_DIR, "libhzg_peak.so")
 SOURCES = ["hzg_api.cu", "hzg_kernels.cu", "hzg_inner.cu", "hzg_dmma.cu", "hzg_tall.cu", "hzg_nccl.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -67,6 +68,11 @@ def build(force=False, verbose=False):
                 sys.stderr.write(msg)
     if force or jobs or _stale(LIB, objs):
         run([nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcuda", "-ldl"])
+    # the FP64 DMMA peak probe bench.py measures its roofline denominator
+    # with (tools/hzg_peak.cu; measurement only, not on the solve path)
+    src = os.path.join(ROOT, "tools", "hzg_peak.cu")
+    if force or _stale(PEAK_LIB, [src]):
+        run([nvcc()] + ARCH + ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-o", PEAK_LIB, src])
     return LIB
 
 
