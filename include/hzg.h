@@ -49,6 +49,7 @@ typedef struct {
   double gate_eps;          /* 2**-52 */
   int32_t exact;            /* 1: reference-order Grammian / postmultiply kernels */
   int32_t split_rows;       /* DMMA Grammian rows per split (multiple of 64); 0 = default geometry */
+  int32_t approx_2x2;       /* exact == 0 only: short-chain 2x2 transforms (tolerance parity) */
 } hzg_config;
 
 typedef struct hzg_ctx hzg_ctx;

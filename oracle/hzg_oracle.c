@@ -1094,3 +1094,13 @@ int hzo_sample_steps(int64_t mF, int64_t mG, int64_t n, int cplx, double* Fr, do
   free(scr); free(stv); free(tv); free(bv); free(buf); free(z0); free(outer); free(inner);
   return st;
 }
+
+/* _k_postmult (blocked.py:220-250) on a stacked m x 2w column pair [Yp Yq]
+ * (column-major, ld m) with the 2w x 2w transform B (column-major); exported
+ * for the single-operation parity test of postmultiply. */
+void hzo_postmult(int64_t m, int w, int cplx, double* Yr, double* Yi, const double* Br, const double* Bi) {
+  plane_t Y = {Yr, Yi, m, 2 * w, m};
+  double* scratch = (double*)malloc(8 * 4 * 2 * w);
+  postmult(Y, 0, w, w, Br, Bi, cplx, scratch);
+  free(scratch);
+}

@@ -21,7 +21,7 @@ class HzgConfig(ctypes.Structure):
                 ("max_inner_sweeps", ctypes.c_int32), ("max_outer_sweeps", ctypes.c_int32),
                 ("block_width", ctypes.c_int32), ("sorting", ctypes.c_int32), ("fallback_qr", ctypes.c_int32),
                 ("shorten_qr", ctypes.c_int32), ("gate_eps", ctypes.c_double), ("exact", ctypes.c_int32),
-                ("split_rows", ctypes.c_int32)]
+                ("split_rows", ctypes.c_int32), ("approx_2x2", ctypes.c_int32)]
 
 
 EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_set_z_rows", "hzg_init_fgz", "hzg_sweep",
@@ -127,7 +127,8 @@ def make_config(cfg):
     return HzgConfig(cfg.variant_id, int(cfg.outer_kind == "mm"), int(cfg.inner_kind == "mm"),
                      cfg.max_inner_sweeps, cfg.max_outer_sweeps, cfg.block_width, int(bool(cfg.sorting)),
                      int(bool(cfg.fallback_qr)), int(cfg.shorten == "qr"), float(cfg.gate_eps),
-                     int(bool(getattr(cfg, "exact", False))), int(getattr(cfg, "split_rows", 0)))
+                     int(bool(getattr(cfg, "exact", False))), int(getattr(cfg, "split_rows", 0)),
+                     int(bool(getattr(cfg, "approx_2x2", True)) and not getattr(cfg, "exact", False)))
 
 
 def check(code, ctx=None, what=""):

@@ -1,11 +1,16 @@
 """Solver configuration (the reference's SolverConfig, pointwise.py:40-81).
 
-Same fields, defaults, decoding and ValueError behaviour.  Two B200-only
+Same fields, defaults, decoding and ValueError behaviour.  Three B200-only
 fields are added:
 
 * ``exact`` selects the reference-order Grammian and postmultiply kernels
   (bitwise agreement with the CPU reference) instead of the FP64
   tensor-core (DMMA) kernels used by default;
+* ``approx_2x2`` (DMMA mode, default on) computes the 2x2 transforms with
+  the short-chain forms (reciprocal square roots of sums of squares instead
+  of the reference's chain of divisions and square roots; tolerance
+  parity, hzg_device.cuh).  Off, or with ``exact``, the 2x2 math is
+  bitwise the reference's;
 * ``split_rows`` (DMMA mode) fixes the rows per Grammian split (a multiple
   of 64, 0 = the default geometry).  The split geometry sets the summation
   order of the block Grammians, so it is part of the configuration, not of
@@ -42,6 +47,7 @@ class SolverConfig:
     pool: int = 1
     exact: bool = False
     split_rows: int = 0
+    approx_2x2: bool = True
     criterion: str = dc_field(init=False, default="C1")
     prescale: bool = dc_field(init=False, default=True)
     compensated: bool = dc_field(init=False, default=False)

@@ -284,6 +284,7 @@ KernelCfg kernel_cfg(const hzg_ctx* c) {
   k.fallback_qr = c->cfg.fallback_qr;
   k.shorten_qr = c->cfg.shorten_qr;
   k.epsn = c->epsn;
+  k.approx_2x2 = !c->cfg.exact && c->cfg.approx_2x2;
   return k;
 }
 

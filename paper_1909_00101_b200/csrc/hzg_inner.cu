@@ -452,17 +452,25 @@ __device__ int block_qr(const Plane& Y, int64_t c0, int64_t c1, int w, double* S
 // _k_process_pivot's scalar part (pointwise.py:165-207) for one pivot:
 // q = {a11, a22, a12r, b11, b22, b12r, a12i, b12i}.  Returns flags (1 applied,
 // 2 big, 4 swap, 8 bad) and, when applied, the rescaled Z-hat entries.
-template <bool CPLX, class M>
+// APPROX: the short-chain 2x2 forms of the DMMA mode (hzg_device.cuh).
+template <bool CPLX, bool APPROX = false, class M>
 __device__ __forceinline__ int pivot_scalar(M& m, const KernelCfg& kc, const double* q, double (&z)[6]) {
   double a11 = q[0], a22 = q[1], a12r = q[2], b11 = q[3], b22 = q[4], b12r = q[5];
   double a12i = CPLX ? q[6] : 0.0, b12i = CPLX ? q[7] : 0.0;
   if (!(a11 > 0.0 && a22 > 0.0 && b11 > 0.0 && b22 > 0.0)) return 8;
   double d11 = 1.0, d22 = 1.0;
   if (kc.per_step_rescale) rescale2(m, a11, a12r, a12i, a22, b11, b12r, b12i, b22, d11, d22);
-  double xb = -1.0;
-  if (gate<CPLX>(m, a11, a12r, a12i, a22, b12r, b12i, kc.epsn, &xb)) return (kc.sorting && a11 < a22) ? 4 : 0;
-  Xform X = CPLX ? transform_cplx(m, a11, a12r, a12i, a22, b12r, b12i, xb)
-                 : transform_real(m, a11, a12r, a22, b12r);
+  Xform X;
+  if constexpr (APPROX) {
+    double x2 = 0.0;
+    if (gate_sq<CPLX>(a11, a12r, a12i, a22, b12r, b12i, kc.epsn, x2, m.ok)) return (kc.sorting && a11 < a22) ? 4 : 0;
+    X = CPLX ? transform_cplx_approx(m, a11, a12r, a12i, a22, b12r, b12i, x2)
+             : transform_real_approx(m, a11, a12r, a22, b12r);
+  } else {
+    double xb = -1.0;
+    if (gate<CPLX>(m, a11, a12r, a12i, a22, b12r, b12i, kc.epsn, &xb)) return (kc.sorting && a11 < a22) ? 4 : 0;
+    X = CPLX ? transform_cplx(m, a11, a12r, a12i, a22, b12r, b12i, xb) : transform_real(m, a11, a12r, a22, b12r);
+  }
   const int bg = kc.crit_c2 ? !(X.cphi == 1.0 && X.cpsi == 1.0) : !(X.z11 == 1.0 && X.z22 == 1.0);
   int flags = 1 | (bg ? 2 : 0);
   if (kc.sorting && !CPLX) {
@@ -494,7 +502,7 @@ struct InnerParams {
 };
 
 template <int TW, bool CPLX, int SW>
-__global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerParams P) {
+__global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPLX) ? 4 : 1) k_inner(InnerParams P) {
   using Geo = InnerGeo<TW, CPLX>;
   constexpr int NPIV = Geo::NPIV;
   constexpr int NW = Geo::NW;  // warps
@@ -762,14 +770,19 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32) k_inner(InnerPara
 #else
         if (mathlane) {
 #endif
-          FastMath fm;
-          flags = pivot_scalar<CPLX>(fm, kc, qv, z);
-          if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
-            IeeeMath im;
-            flags = pivot_scalar<CPLX>(im, kc, qv, z);
-#ifdef HZG_EXP_FALLBACK
-            if (P.io.phase) atomicAdd((unsigned long long*)&P.io.phase[0], 1000000000ull);
-#endif
+          bool exact_path = true;
+          if (kc.approx_2x2) {
+            FastMath fm;
+            flags = pivot_scalar<CPLX, true>(fm, kc, qv, z);
+            exact_path = !fm.ok;  // out of the short forms' range: the reference-order path
+          }
+          if (exact_path) {
+            FastMath fm;
+            flags = pivot_scalar<CPLX>(fm, kc, qv, z);
+            if (!fm.ok) {  // an operand left the fast paths' range: redo with IEEE operators
+              IeeeMath im;
+              flags = pivot_scalar<CPLX>(im, kc, qv, z);
+            }
           }
           if (flags & 1) {
             lane_applied += 1;

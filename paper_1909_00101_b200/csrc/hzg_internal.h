@@ -44,6 +44,7 @@ struct KernelCfg {
   int fallback_qr;
   int shorten_qr;       // cfg.shorten == "qr": QR R factors instead of Grammian + Cholesky
   double epsn;          // gate_eps * sqrt(n) (blocked.py:571-572)
+  int approx_2x2;       // DMMA mode: short-chain 2x2 forms (tolerance parity); 0: reference order
 };
 
 // Grammian partials: [pair][mat(F,G)][split][plane][tw*tw], element (r,s) at s*tw+r.

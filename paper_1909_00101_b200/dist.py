@@ -336,7 +336,10 @@ class PartitionedGsvd:
         w = cfg.block_width
         n = planes["Fr"].shape[0]
         self.nblk = n // w
-        self.nranks = max(1, min(nranks, self.nblk // 2))
+        if not 1 <= nranks <= self.nblk // 2:
+            raise ValueError("%d ranks for %d column blocks: the block-partitioned schedule needs "
+                             "1 <= ranks <= blocks / 2" % (nranks, self.nblk))
+        self.nranks = nranks
         self.sched = BlockSchedule(self.nblk, self.nranks)
         epsn = epsn_of(cfg, n)
         self.comm = comm

@@ -84,7 +84,7 @@ def _gpu_block(tw, cplx, cfg, epsn, grams):
 @pytest.mark.parametrize("cplx", [False, True])
 @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5, 6, 7])
 def test_inner_block_kernel_bitwise(tw, cplx, variant):
-    cfg = hz.SolverConfig(variant_id=variant, block_width=tw // 2)
+    cfg = hz.SolverConfig(variant_id=variant, block_width=tw // 2, approx_2x2=False)
     epsn = EPS * np.sqrt(1024.0)
     for seed in range(3):
         grams = _random_grams(tw, cplx, 1000 * tw + seed)
@@ -103,7 +103,7 @@ def test_inner_block_kernel_bitwise(tw, cplx, variant):
 @pytest.mark.parametrize("kw", [dict(sorting=False), dict(inner_kind="mm"), dict(blocking="bo")])
 def test_inner_block_kernel_bitwise_options(kw):
     tw = 32
-    cfg = hz.SolverConfig(block_width=16, **kw)
+    cfg = hz.SolverConfig(block_width=16, approx_2x2=False, **kw)
     epsn = EPS * np.sqrt(4096.0)
     for cplx in (False, True):
         grams = _random_grams(tw, cplx, 77)
@@ -114,6 +114,30 @@ def test_inner_block_kernel_bitwise_options(kw):
         Zg, cnt = _gpu_block(tw, cplx, cfg, epsn, grams)
         assert (cnt[0], cnt[1], cnt[2]) == (tot, big, 0)
         assert np.array_equal(Zg, Zo)
+
+
+@pytest.mark.parametrize("tw", [2, 8, 16, 32, 64])
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("variant", [0, 3, 4, 6])
+def test_inner_block_kernel_approx_2x2_vs_oracle(tw, cplx, variant):
+    """The short-chain 2x2 forms (DMMA mode): the block solve's transform
+    Z~ agrees with the oracle's to rounding -- ||Z~ - Z~_ref||_max <= 64 tw
+    eps ||Z~_ref||_max -- and applies the same number of transforms up to
+    boundary cases of the gate (within 2 %)."""
+    cfg = hz.SolverConfig(variant_id=variant, block_width=tw // 2)
+    assert cfg.approx_2x2
+    epsn = EPS * np.sqrt(1024.0)
+    for seed in range(3):
+        grams = _random_grams(tw, cplx, 2000 * tw + seed)
+        (Fr, Fi), (Gr, Gi) = grams
+        Fh, _ = O.cholesky_upper(Fr + 1j * Fi if cplx else Fr)
+        Gh, _ = O.cholesky_upper(Gr + 1j * Gi if cplx else Gr)
+        _, _, Zo, tot, big, st = O.block_inner(Fh, Gh, O.cfg_from(cfg), epsn)
+        Zg, cnt = _gpu_block(tw, cplx, cfg, epsn, grams)
+        assert cnt[2] == 0
+        assert abs(int(cnt[0]) - tot) <= max(2, 0.02 * tot), (cnt, tot)
+        err = np.abs(Zg - Zo).max() / np.abs(Zo).max()
+        assert err <= 64 * tw * EPS, (tw, cplx, variant, seed, err)
 
 
 def test_inner_block_kernel_not_pd_signal():
@@ -274,8 +298,8 @@ def test_block_partitioned_ranks_bitwise_equal_single(name, exact):
     cfg = _cfg(c, exact=exact)
     one = hz.solve(c["F"], c["G"], cfg)
     for ranks in (2, 3, 4):
-        r = hz.solve(c["F"], c["G"], cfg, workers=ranks)
-        assert r.workers <= ranks
+        r = hz.solve(c["F"], c["G"], cfg, workers=ranks, scheme="blocks")
+        assert r.workers == ranks
         assert (r.sweeps, r.total_transforms, r.big_transforms) == (one.sweeps, one.total_transforms,
                                                                     one.big_transforms)
         for a, b in ((r.sigma, one.sigma), (r.U.re, one.U.re), (r.V.re, one.V.re), (r.Z.re, one.Z.re)):
@@ -290,7 +314,7 @@ def test_block_partitioned_1024_eight_ranks():
     G = g[1024 * 1024:].reshape((1024, 1024), order="F")
     cfg = hz.SolverConfig(block_width=16)
     one = hz.solve(F, G, cfg)
-    r = hz.solve(F, G, cfg, workers=8)
+    r = hz.solve(F, G, cfg, workers=8, scheme="blocks")
     assert r.workers == 8
     assert np.array_equal(r.sigma, one.sigma) and np.array_equal(r.Z.re, one.Z.re)
 
