@@ -775,6 +775,8 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPL
             FastMath fm;
             flags = pivot_scalar<CPLX, true>(fm, kc, qv, z);
             exact_path = !fm.ok;  // out of the short forms' range: the reference-order path
+            // diagnostics (hzg_debug_phases): count the fallbacks in units of 1e9 in slot 0
+            if (exact_path && P.io.phase) atomicAdd((unsigned long long*)&P.io.phase[0], 1000000000ull);
           }
           if (exact_path) {
             FastMath fm;
