@@ -230,6 +230,27 @@ int hzg_comm_exchange(hzg_ctx* ctx, const int32_t* moves, int32_t count);
 /* Destroy the communicator (hzg_destroy does it too). */
 int hzg_comm_detach(hzg_ctx* ctx);
 
+/* ---- accuracy check (the reference's accuracy_report, harness.py:323-465) */
+
+/* In-place LU with complete pivoting of the n x n column-major planes A
+ * (ld >= n): _k_lu_complete (harness.py:323-371), bitwise the reference's
+ * factors.  rp, cp (device int64[n]) must hold 0..n-1 on entry and receive
+ * the row / column permutations; *status (device) = 1 on a zero pivot.
+ * workspace: hzg_lu_workspace_bytes(n) bytes.  Asynchronous on `stream`. */
+size_t hzg_lu_workspace_bytes(int64_t n);
+int hzg_lu_complete(int64_t n, int32_t is_complex, double* Ar, double* Ai, int64_t ld, int64_t* rp, int64_t* cp,
+                    void* workspace, int32_t* status, void* stream);
+/* C = op(A) B (op(A) = A, or A^H with trans_a), every entry a compensated
+ * dot product (matmul_compensated, harness.py:151-196). */
+int hzg_gemm_comp(int64_t m, int64_t n, int64_t k, int32_t is_complex, int32_t trans_a, const double* Ar,
+                  const double* Ai, int64_t lda, const double* Br, const double* Bi, int64_t ldb, double* Cr,
+                  double* Ci, int64_t ldc, void* stream);
+/* Compensated sum of |A - B|^2 (B null: |A|^2; eye: B = I) over rows x cols,
+ * as nblocks (sum, error) pairs in partials[2 * nblocks] (_frob_comp,
+ * harness.py:208-216). */
+int hzg_sumsq_comp(int64_t rows, int64_t cols, const double* Ar, const double* Ai, int64_t lda, const double* Br,
+                   const double* Bi, int64_t ldb, int32_t eye, double* partials, int32_t nblocks, void* stream);
+
 const char* hzg_last_error(const hzg_ctx* ctx);
 void hzg_destroy(hzg_ctx* ctx);
 

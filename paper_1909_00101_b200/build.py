@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libhzg.so")
 PEAK_LIB = os.path.join(OUT_DIR, "libhzg_peak.so")
-SOURCES = ["hzg_api.cu", "hzg_kernels.cu", "hzg_inner.cu", "hzg_dmma.cu", "hzg_tall.cu", "hzg_nccl.cu"]
+SOURCES = ["hzg_api.cu", "hzg_kernels.cu", "hzg_inner.cu", "hzg_dmma.cu", "hzg_tall.cu", "hzg_nccl.cu", "hzg_accuracy.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

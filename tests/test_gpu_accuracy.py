@@ -1,0 +1,97 @@
+"""The device accuracy report (accuracy.py, hzg_lu_complete / hzg_gemm_comp /
+hzg_sumsq_comp) against the reference's own accuracy_report on the same
+results (tests/golden/make_accuracy_golden.py runs the reference):
+
+* the complete-pivoting LU of Z: factors and permutations bitwise the
+  reference's _k_lu_complete (harness.py:323-371);
+* X = Z^{-1} within 1e-12 of the reference's (different substitution order);
+* resF, resG, orthU, orthV within 5 % (or 2e-16 absolute) of the reference's
+  values -- both are compensated measurements of the same quantities.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_1909_00101_b200 as hz
+from paper_1909_00101_b200 import _native
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+CASES = ["corpus64_real_w16", "corpus64_complex_w16", "gauss200_w16"]
+
+
+def _load(name):
+    return dict(np.load(os.path.join(GOLDEN, "acc_%s.npz" % name)))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_lu_complete_bitwise_vs_reference(name):
+    import torch
+    c = _load(name)
+    Z = c["Z"]
+    cplx = np.iscomplexobj(Z)
+    n = Z.shape[0]
+    dev = torch.device("cuda")
+    Ar = torch.from_numpy(np.ascontiguousarray(Z.real.T)).to(dev)
+    Ai = torch.from_numpy(np.ascontiguousarray(Z.imag.T)).to(dev) if cplx else None
+    rp = torch.arange(n, dtype=torch.int64, device=dev)
+    cp = torch.arange(n, dtype=torch.int64, device=dev)
+    L = _native.load()
+    ws = torch.empty(int(L.hzg_lu_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+    assert L.hzg_lu_complete(n, int(cplx), P(Ar), P(Ai), n, P(rp), P(cp), P(ws), P(st),
+                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert np.array_equal(rp.cpu().numpy(), c["rp"]) and np.array_equal(cp.cpu().numpy(), c["cp"])
+    assert np.array_equal(Ar.cpu().numpy().T, c["LUr"])
+    if cplx:
+        assert np.array_equal(Ai.cpu().numpy().T, c["LUi"])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_accuracy_report_vs_reference(name):
+    import torch
+    c = _load(name)
+    Z = c["Z"]
+    cplx = np.iscomplexobj(Z)
+    dev = torch.device("cuda")
+    Xr, Xi = hz.invert_via_lu(torch.from_numpy(np.ascontiguousarray(Z.real.T)).to(dev),
+                              torch.from_numpy(np.ascontiguousarray(Z.imag.T)).to(dev) if cplx else None)
+    X = Xr.cpu().numpy().T + (1j * Xi.cpu().numpy().T if cplx else 0)
+    assert np.abs(X - c["X"]).max() <= 1e-12 * np.abs(c["X"]).max()
+    M = hz.MatrixPlanePair.from_dense
+    p = hz.ProblemPair(M(c["F"]), M(c["G"]))
+    r = hz.GsvdResult(M(c["U"]), M(c["V"]), M(Z), c["sigmaF"], c["sigmaG"], c["sigma"], sweeps=0,
+                      total_transforms=0, big_transforms=0)
+    rep = hz.accuracy_report(p, r, reference=c["sigma"])
+    got = np.array([rep.resF, rep.resG, rep.orthU, rep.orthV])
+    want = c["report"]
+    assert np.all(np.abs(got - want) <= np.maximum(0.05 * want, 2e-16)), (got, want)
+    assert rep.max_rel_sigma == 0.0
+
+
+def test_accuracy_report_on_a_solve():
+    """The report of a device solve meets the reference's acceptance bounds
+    (test_acceptance.py:110-130: resF/resG <= 1e-12, ||U^H U - I|| <= n 1e-14)."""
+    c = _load("gauss200_w16")
+    F, G = c["F"], c["G"]
+    r = hz.solve(F, G, hz.SolverConfig(block_width=16))
+    p = hz.ProblemPair(hz.MatrixPlanePair.from_dense(F), hz.MatrixPlanePair.from_dense(G))
+    rep = hz.accuracy_report(p, r, reference=c["sigma"])
+    n = F.shape[1]
+    assert rep.resF <= 1e-12 and rep.resG <= 1e-12
+    assert rep.orthU <= n * 1e-14 and rep.orthV <= n * 1e-14
+    assert rep.max_rel_sigma <= 8 * n * 2.0 ** -52
+
+
+def test_singular_z_raises():
+    import torch
+    Z = torch.zeros((8, 8), dtype=torch.float64, device="cuda")
+    Z[0, 0] = 1.0
+    with pytest.raises(hz.NotPositiveDefiniteError):
+        hz.invert_via_lu(Z)
