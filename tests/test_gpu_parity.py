@@ -447,7 +447,7 @@ def test_pivot_property_many_random_2x2(cplx):
     (the reference's kernel property suites, test_acceptance.py:267-290,
     test_kernel2x2.py:167-203)."""
     rng = np.random.default_rng(2024 + cplx)
-    cfg = hz.SolverConfig(block_width=1)
+    cfg = hz.SolverConfig(block_width=1, approx_2x2=False)
     epsn = EPS * np.sqrt(64.0)
     for t in range(400):
         m = 3
