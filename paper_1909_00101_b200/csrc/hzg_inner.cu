@@ -768,7 +768,12 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPL
         }
         if (false) {
 #else
-        if (mathlane) {
+        // Without compensation every lane of the group already holds the
+        // eight sums (the gather above is a broadcast), so all of them run
+        // the pivot's 2x2 math -- the same instructions the math lane alone
+        // would issue -- and nobody waits for a broadcast of the results.
+        const bool redundant = !kc.compensated;
+        if (redundant ? valid : mathlane) {
 #endif
           bool exact_path = true;
           if (kc.approx_2x2) {
@@ -776,7 +781,8 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPL
             flags = pivot_scalar<CPLX, true>(fm, kc, qv, z);
             exact_path = !fm.ok;  // out of the short forms' range: the reference-order path
             // diagnostics (hzg_debug_phases): count the fallbacks in units of 1e9 in slot 0
-            if (exact_path && P.io.phase) atomicAdd((unsigned long long*)&P.io.phase[0], 1000000000ull);
+            if (exact_path && P.io.phase && sub == 0)
+              atomicAdd((unsigned long long*)&P.io.phase[0], 1000000000ull);
           }
           if (exact_path) {
             FastMath fm;
@@ -786,15 +792,20 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPL
               flags = pivot_scalar<CPLX>(im, kc, qv, z);
             }
           }
-          if (flags & 1) {
+          if ((flags & 1) && sub == 0) {
             lane_applied += 1;
             lane_big += (flags >> 1) & 1;
           }
         }
         const int bad = flags & 8;
-        flags = __shfl_sync(0xffffffffu, flags, base);
+#ifndef HZG_EXP_NOMATH
+        if (!redundant)
+#endif
+        {
+          flags = __shfl_sync(0xffffffffu, flags, base);
 #pragma unroll
-        for (int c = 0; c < 6; ++c) z[c] = __shfl_sync(0xffffffffu, z[c], base);
+          for (int c = 0; c < 6; ++c) z[c] = __shfl_sync(0xffffffffu, z[c], base);
+        }
         if (st == P.isteps - 1) {
           int sa = lane_applied, sb = lane_big;
 #pragma unroll
