@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--size", dest="n", type=int, default=16384, help="matrix order n (config 5: 16384)")
     ap.add_argument("--kind", default="gauss", choices=["cond", "gauss"],
                     help="gauss: iid Gaussian (config 5); cond: config 4 (sigma in [1e-8, 1e8])")
-    ap.add_argument("--w", type=int, default=16)
+    ap.add_argument("--w", type=int, default=32,
+                    help="block width (config 5 default 32: 30 vs 42 sweeps to convergence at n = 16384 with w = 16)")
     ap.add_argument("--seed", type=int, default=4096)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--e2e-sweeps", type=int, default=2)
@@ -580,23 +581,36 @@ def main():
             tj = json.load(fh)
         traffic = tj.get("postmult_dram_bytes_per_launch")
         gram_traffic = tj.get("grammian_dram_bytes_per_launch")
-    roofline = {"kernel": "k_post_ws (postmultiply of F, G, Z block pairs; the dominant HBM-bound kernel)",
-                "bound": "hbm", "achieved": post_gbs, "peak": hbm_peak, "unit": "GB/s",
-                "frac": post_gbs / hbm_peak, "traffic": traffic,
+    peak_tf, peak_info = fp64_peak(local)
+    npairs = n // w // 2
+    fpl = {"postmult": npairs * 8 * w * w * (mF + mG + n), "grammian": npairs * 4 * w * w * (mF + mG)}
+    post_tf = fpl["postmult"] / (avg["postmult"] / 1e3) / 1e12
+    gram_tf = fpl["grammian"] / (avg["grammian"] / 1e3) / 1e12
+    # the dominant kernel's bound: HBM at 2w <= 32 (4 flop/B), the FP64
+    # tensor pipe at 2w = 64 (8 flop/B > the ~5.7 flop/B ridge)
+    post_tensor = post_tf / peak_tf > post_gbs / hbm_peak
+    roofline = {"kernel": "k_post_ws (postmultiply of the F, G, Z block pairs of one outer step; the dominant kernel)",
+                "bound": "tensor" if post_tensor else "hbm",
+                "achieved": post_tf if post_tensor else post_gbs, "peak": peak_tf if post_tensor else hbm_peak,
+                "unit": "TFLOP/s" if post_tensor else "GB/s",
+                "frac": post_tf / peak_tf if post_tensor else post_gbs / hbm_peak, "traffic": traffic,
                 "traffic_note": ("DRAM bytes per launch, ncu --set full (profiles/traffic_w%d_n%d.json)" % (w, n))
                 if traffic else None,
-                "peak_source": peak_src,
-                "bytes_per_launch": bpl["postmult"], "avg_launch_ms": avg["postmult"],
+                "peak_source": ("FP64 DMMA peak measured now (tools/hzg_peak.cu)" if post_tensor else peak_src),
+                "bytes_per_launch": bpl["postmult"], "flops_per_launch": fpl["postmult"],
+                "avg_launch_ms": avg["postmult"],
+                "hbm": {"achieved": post_gbs, "peak": hbm_peak, "frac": post_gbs / hbm_peak},
+                "tensor": {"achieved_tflops": post_tf, "peak_tflops": peak_tf, "frac": post_tf / peak_tf},
                 "measured": "isolated: sweep 1 of this pair, one launch per outer step covering all %d pairs, "
-                            "CUDA events on the launch stream" % (n // w // 2),
-                "grammian": {"achieved": gram_gbs, "frac": gram_gbs / hbm_peak, "bytes_per_launch": bpl["grammian"],
+                            "CUDA events on the launch stream" % npairs,
+                "grammian": {"achieved_gbs": gram_gbs, "hbm_frac": gram_gbs / hbm_peak,
+                             "achieved_tflops": gram_tf, "tensor_frac": gram_tf / peak_tf,
+                             "bytes_per_launch": bpl["grammian"], "flops_per_launch": fpl["grammian"],
                              "avg_launch_ms": avg["grammian"], "traffic": gram_traffic},
-                "inner": {"avg_launch_ms": avg["inner"], "bound": "latency (dependent FP64 div/sqrt chains + "
-                                                                 "one CTA barrier per inner step)"},
+                "inner": {"avg_launch_ms": avg["inner"], "bound": "latency (dependent FP64 rsqrt / div chains of "
+                                                                 "the 2x2 math + one CTA barrier per inner step)"},
                 "kernel_time_shares_isolated": {k: v[0] / tot_k for k, v in kt.items()} if tot_k else {},
                 "timed_region_hbm_gbs": a.steps * sweep_bytes(n, mF, mG, w) / (ms_max / 1e3) / 1e9}
-
-    peak_tf, peak_info = fp64_peak(local)
     roofline["fp64"] = {"achieved_tflops": value / 1e3, "peak_tflops": peak_tf, "peak": peak_info,
                         "frac": value / 1e3 / peak_tf}
     if full and "gflops" in full:
@@ -604,7 +618,8 @@ def main():
 
     extra = None
     if world == 1 and a.config4_size > 0:
-        extra = config4_full(hz, torch, device, a.config4_size, w, 4096, peak_tf)
+        # config 4 at w = 16: 8.3 s vs 8.5 s at w = 32 (inner-solve bound at n = 4096)
+        extra = config4_full(hz, torch, device, a.config4_size, 16, 4096, peak_tf)
 
     cpu = None
     if not a.no_cpu and world == 1:

@@ -555,11 +555,8 @@ void set_smem(K k, size_t bytes) {
 template <int TW, bool CPLX>
 int gram_ws_t(const GramParams& p, cudaStream_t s) {
   using C = GramWsCfg<TW, CPLX>;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_gram_ws<TW, CPLX>, C::SMEM);
-    once = true;
-  }
+  static PerDeviceOnce once;
+  if (once.first()) set_smem(k_gram_ws<TW, CPLX>, C::SMEM);
   dim3 grid(p.sp.pn, 2, p.gw.smax);
   k_gram_ws<TW, CPLX><<<grid, 160, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
@@ -568,11 +565,8 @@ int gram_ws_t(const GramParams& p, cudaStream_t s) {
 template <int TW, bool CPLX>
 int post_ws_t(const PostParams& p, int64_t mmax, int nmats, cudaStream_t s) {
   using C = PostWsCfg<TW, CPLX>;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_post_ws<TW, CPLX>, C::SMEM);
-    once = true;
-  }
+  static PerDeviceOnce once;
+  if (once.first()) set_smem(k_post_ws<TW, CPLX>, C::SMEM);
   dim3 grid(p.sp.pn, nmats, (unsigned)((mmax + p.chunk - 1) / p.chunk));
   k_post_ws<TW, CPLX><<<grid, 160, C::SMEM, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
@@ -587,11 +581,8 @@ bool postgram_supported(int w, int cplx) { return w == 16 && !cplx; }
 int launch_postgram(const Plane& F, const Plane& G, const StepPairs& sp, int step, int w, int cplx,
                     const InnerOut& io, const GramWS& gw, const PostGramTables& t, cudaStream_t s) {
   if (!postgram_supported(w, cplx)) return 4;
-  static bool once = false;
-  if (!once) {
-    set_smem(k_postgram, PGCfg::SMEM);
-    once = true;
-  }
+  static PerDeviceOnce once;
+  if (once.first()) set_smem(k_postgram, PGCfg::SMEM);
   PostGramParams p{{F, G}, sp, step, io, gw, t};
   dim3 grid(t.nchains, gw.smax, 2);
   k_postgram<<<grid, 160, PGCfg::SMEM, s>>>(p);
@@ -626,12 +617,7 @@ int launch_postmult_dmma(const Plane& F, const Plane& G, const Plane& Z, const S
   // per SM (fewer, longer CTAs stream better at n = 16384: 20.33 vs 19.96
   // TFLOP/s with 4096 vs 1024; n = 4096 keeps 1024); HZG_POST_CHUNK
   // overrides (multiple of 64).  Row chunking does not change any output bit.
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-  }
+  const int sms = device_sms();
   int64_t chunk = 1024;
   while (chunk < 4096 && (int64_t)sp.npairs * ((mmax + 2 * chunk - 1) / (2 * chunk)) * nmats >= 2 * sms) chunk *= 2;
   if (const char* e = std::getenv("HZG_POST_CHUNK")) chunk = std::max(64, std::atoi(e)) / 64 * 64;

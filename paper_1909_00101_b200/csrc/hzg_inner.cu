@@ -12,6 +12,7 @@
 // counters are bitwise those of the reference's _block_task
 // (blocked.py:435-484; pointwise.py:161-293).
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 
@@ -502,7 +503,8 @@ struct InnerParams {
 };
 
 template <int TW, bool CPLX, int SW>
-__global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPLX) ? 4 : 1) k_inner(InnerParams P) {
+__global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPLX) ? 4 : ((TW == 64 && !CPLX) ? 2 : 1))
+k_inner(InnerParams P) {
   using Geo = InnerGeo<TW, CPLX>;
   constexpr int NPIV = Geo::NPIV;
   constexpr int NW = Geo::NW;  // warps
@@ -1011,12 +1013,13 @@ __global__ void __launch_bounds__(InnerGeo<TW, CPLX>::NW * 32, (TW <= 32 && !CPL
 
 template <int TW, bool CPLX, int SW>
 int launch_inner_g(const InnerParams& p, cudaStream_t s) {
-  const size_t smem = sizeof(InnerSmem<TW, CPLX>);
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_inner<TW, CPLX, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_done = true;
-  }
+  // the compensated variants' scratch (cbuf, the struct's last member) is
+  // only allocated when they run: 2w = 64 real then fits 2 CTAs per SM
+  using Smem = InnerSmem<TW, CPLX>;
+  const size_t full = sizeof(Smem);
+  const size_t smem = p.kc.compensated ? full : offsetof(Smem, cbuf);
+  static PerDeviceOnce attr;
+  if (attr.first()) cudaFuncSetAttribute(k_inner<TW, CPLX, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)full);
   // HZG_INNER_CTAS caps the CTAs of one launch (each then serves several
   // pairs), leaving SM room for the streaming kernels of other groups
   static int cap = -1;

@@ -5,6 +5,30 @@
 
 namespace hzg {
 
+// Kernel attributes (dynamic shared memory limits) are per device: a call
+// site sets them the first time it runs on each device of the process.
+struct PerDeviceOnce {
+  unsigned long long done = 0;  // bit d: device d (d < 64) done
+  bool first() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long b = 1ull << (d & 63);
+    if (done & b) return false;
+    done |= b;
+    return true;
+  }
+};
+
+// SM count of the current device (cached per device)
+inline int device_sms() {
+  static int sms[64] = {0};
+  int d = 0;
+  cudaGetDevice(&d);
+  int& v = sms[d & 63];
+  if (v <= 0 && (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0)) v = 148;
+  return v;
+}
+
 // status bits written per block pair (and OR-folded per sweep)
 enum : int {
   ST_OK = 0,

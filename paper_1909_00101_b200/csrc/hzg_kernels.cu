@@ -300,11 +300,9 @@ template <int TW, bool CPLX>
 int launch_post_exact_t(const PostExactParams& p, int64_t mmax, cudaStream_t s) {
   dim3 grid((unsigned)((mmax + 127) / 128), p.sp.pn, 3);
   const size_t smem = (CPLX ? 2 : 1) * TW * TW * sizeof(double);
-  static bool once = false;
-  if (!once) {
+  static PerDeviceOnce once;
+  if (once.first())
     cudaFuncSetAttribute(k_postmult_exact<TW, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    once = true;
-  }
   k_postmult_exact<TW, CPLX><<<grid, 128, smem, s>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
