@@ -87,7 +87,7 @@ struct GramWsCfg {
 };
 
 template <int TW, bool CPLX>
-__global__ void __launch_bounds__(160) k_gram_ws(GramParams P) {
+__global__ void __launch_bounds__(160, (TW == 64 && !CPLX) ? 2 : 1) k_gram_ws(GramParams P) {
   using C = GramWsCfg<TW, CPLX>;
   constexpr int NP = C::NP, NT = C::NT, NTILE = C::NTILE;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -550,6 +550,9 @@ __global__ void __launch_bounds__(160) k_postgram(PostGramParams P) {
 template <typename K>
 void set_smem(K k, size_t bytes) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  // the whole unified L1 / shared array as shared memory: two ~105 KB
+  // stage rings per SM at 2w = 64
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 template <int TW, bool CPLX>

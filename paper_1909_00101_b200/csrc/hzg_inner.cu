@@ -673,7 +673,11 @@ k_inner(InnerParams P) {
     const bool valid = NPIV % PG == 0 || pv < NPIV;
     const bool mathlane = sub == 0 && valid;
     const bool prof = P.io.phase != nullptr && blockIdx.x == 0 && tid == 0;
-    long long tA = 0, tB = 0, tC = 0, nstep = 0, c0 = 0, c1 = 0;
+    // phase profiling (hzg_debug_phases; thread 0 of CTA 0 only): cycles go
+    // straight to global counters, so production runs carry one register
+    // pair (c0) for it, not six
+    unsigned long long* const ph = prof ? reinterpret_cast<unsigned long long*>(P.io.phase) : nullptr;
+    long long c0 = 0;
     for (int sw = 0; sw < kc.max_inner_sweeps; ++sw) {
       int lane_applied = 0, lane_big = 0;  // math lanes: the pivot's counts this sweep
       int ni_ = valid ? S.tab[pv * 2] : 0, nj_ = valid ? S.tab[pv * 2 + 1] : 1;
@@ -754,8 +758,8 @@ k_inner(InnerParams P) {
         }
         }
         if (prof) {
-          c1 = clock64();
-          tA += c1 - c0;
+          const long long c1 = clock64();
+          atomicAdd(&ph[0], (unsigned long long)(c1 - c0));
           c0 = c1;
         }
         // ---- phase B: _k_process_pivot's scalar part (pointwise.py:165-207)
@@ -821,8 +825,8 @@ k_inner(InnerParams P) {
           }
         }
         if (prof) {
-          c1 = clock64();
-          tB += c1 - c0;
+          const long long c1 = clock64();
+          atomicAdd(&ph[1], (unsigned long long)(c1 - c0));
           c0 = c1;
         }
         // ---- phase C: _k_update_cols / swaps (pointwise.py:178-218)
@@ -919,8 +923,8 @@ k_inner(InnerParams P) {
         // a rank-deficient pivot anywhere ends the solve (RankError upstream)
         const int anybad = __syncthreads_or(bad);
         if (prof) {
-          tC += clock64() - c0;
-          ++nstep;
+          atomicAdd(&ph[2], (unsigned long long)(clock64() - c0));
+          atomicAdd(&ph[3], 1ull);
         }
         if (anybad) {
           status = ST_RANK;
@@ -938,12 +942,6 @@ k_inner(InnerParams P) {
       if (s_cnt == 0) break;
       total += s_cnt;
       big += b_cnt;
-    }
-    if (prof) {
-      P.io.phase[0] += tA;
-      P.io.phase[1] += tB;
-      P.io.phase[2] += tC;
-      P.io.phase[3] += nstep;
     }
   }
 
