@@ -722,27 +722,31 @@ k_inner(InnerParams P) {
         } else {
         double v[8];
         {
-          double p[8][RPL];
-#pragma unroll
-          for (int e = 0; e < RPL; ++e) {
-            p[0][e] = nrm_term<CPLX>(fi[e], fii[e]);
-            p[1][e] = nrm_term<CPLX>(fj[e], fji[e]);
-            p[3][e] = nrm_term<CPLX>(gi[e], gii[e]);
-            p[4][e] = nrm_term<CPLX>(gj[e], gji[e]);
-            if (CPLX) {
-              p[2][e] = dot_re_term(fi[e], fii[e], fj[e], fji[e]);
-              p[6][e] = dot_im_term(fi[e], fii[e], fj[e], fji[e]);
-              p[5][e] = dot_re_term(gi[e], gii[e], gj[e], gji[e]);
-              p[7][e] = dot_im_term(gi[e], gii[e], gj[e], gji[e]);
-            } else {
-              p[2][e] = fi[e] * fj[e];
-              p[5][e] = gi[e] * gj[e];
-              p[6][e] = 0.0;
-              p[7][e] = 0.0;
-            }
+          // one quantity at a time: its RPL products, then its row tree
+          // (each tree's shape is fixed, so the order across quantities
+          // changes no bit, and only RPL products are live at once)
+          double p[RPL];
+#define HZG_SUM(c, expr)                                                  \
+  {                                                                       \
+    _Pragma("unroll") for (int e = 0; e < RPL; ++e) p[e] = (expr);        \
+    v[c] = row_tree<RPL>(p);                                              \
+  }
+          HZG_SUM(0, (nrm_term<CPLX>(fi[e], fii[e])));
+          HZG_SUM(1, (nrm_term<CPLX>(fj[e], fji[e])));
+          HZG_SUM(3, (nrm_term<CPLX>(gi[e], gii[e])));
+          HZG_SUM(4, (nrm_term<CPLX>(gj[e], gji[e])));
+          if (CPLX) {
+            HZG_SUM(2, (dot_re_term(fi[e], fii[e], fj[e], fji[e])));
+            HZG_SUM(6, (dot_im_term(fi[e], fii[e], fj[e], fji[e])));
+            HZG_SUM(5, (dot_re_term(gi[e], gii[e], gj[e], gji[e])));
+            HZG_SUM(7, (dot_im_term(gi[e], gii[e], gj[e], gji[e])));
+          } else {
+            HZG_SUM(2, (fi[e] * fj[e]));
+            HZG_SUM(5, (gi[e] * gj[e]));
+            v[6] = 0.0;
+            v[7] = 0.0;
           }
-#pragma unroll
-          for (int c = 0; c < 8; ++c) v[c] = row_tree<RPL>(p[c]);
+#undef HZG_SUM
         }
         HalvingTree<8, 0, Geo::HL>::run(v, lane);
 #pragma unroll
@@ -830,6 +834,42 @@ k_inner(InnerParams P) {
           c0 = c1;
         }
         // ---- phase C: _k_update_cols / swaps (pointwise.py:178-218)
+        if constexpr (!CPLX) {
+          // real: the swap is decided (flags & 4), so F and G go back to
+          // shared memory before Z's rows are loaded -- fewer live registers
+          if (flags & 5) {
+            const bool swap = (flags & 4) != 0;
+            const int di = swap ? j : i, dj = swap ? i : j;
+            const double z11 = z[0], z12 = z[1], z21 = z[3], z22 = z[5];
+            if (flags & 1) {
+#pragma unroll
+              for (int e = 0; e < RPL; ++e) {
+                const double a = fi[e], b = fj[e], c = gi[e], d = gj[e];
+                fi[e] = fma(b, z21, a * z11);
+                fj[e] = fma(a, z12, b * z22);
+                gi[e] = fma(d, z21, c * z11);
+                gj[e] = fma(c, z12, d * z22);
+              }
+            }
+            store_rows<TW, VEC, RPL, SW>(Ar, di, r0, fi);
+            store_rows<TW, VEC, RPL, SW>(Ar, dj, r0, fj);
+            store_rows<TW, VEC, RPL, SW>(Br, di, r0, gi);
+            store_rows<TW, VEC, RPL, SW>(Br, dj, r0, gj);
+            double zi_[RPL], zj_[RPL];
+            load_rows<TW, VEC, RPL, SW>(Zr, i, r0, zi_);
+            load_rows<TW, VEC, RPL, SW>(Zr, j, r0, zj_);
+            if (flags & 1) {
+#pragma unroll
+              for (int e = 0; e < RPL; ++e) {
+                const double a = zi_[e], b = zj_[e];
+                zi_[e] = fma(b, z21, a * z11);
+                zj_[e] = fma(a, z12, b * z22);
+              }
+            }
+            store_rows<TW, VEC, RPL, SW>(Zr, di, r0, zi_);
+            store_rows<TW, VEC, RPL, SW>(Zr, dj, r0, zj_);
+          }
+        } else {
         bool swap = (flags & 4) != 0;
         double zi_[RPL], zj_[RPL], zii[RPL], zji[RPL];
         if (flags & 5) {
@@ -919,6 +959,7 @@ k_inner(InnerParams P) {
             store_rows<TW, VEC, RPL, SW>(Zi, di, r0, zii);
             store_rows<TW, VEC, RPL, SW>(Zi, dj, r0, zji);
           }
+        }
         }
         // a rank-deficient pivot anywhere ends the solve (RankError upstream)
         const int anybad = __syncthreads_or(bad);
