@@ -72,13 +72,25 @@ def form_grammians(Fp, Fq, Gp, Gq, compensated=False):
     return A, B
 
 
+# block orders the device block kernels are instantiated for (2w; hzg_inner.cu)
+BLOCK_ORDERS = (2, 4, 6, 8, 10, 12, 14, 16, 20, 24, 32, 48, 64)
+
+
+def _check_order(tw, what):
+    if tw not in BLOCK_ORDERS:
+        raise ValueError("%s: order %d is not supported on the device (2w in %s)" % (what, tw, BLOCK_ORDERS))
+
+
 def cholesky_upper(M):
     """Upper Cholesky factor with positive real diagonal (blocked.py:350-355);
     NotPositiveDefiniteError when the factorization breaks down."""
-    torch = _torch()
     M = np.array(M)
     cplx = np.iscomplexobj(M)
     tw = M.shape[0]
+    if M.ndim != 2 or M.shape[1] != tw:
+        raise ValueError("cholesky_upper needs a square matrix")
+    _check_order(tw, "cholesky_upper")
+    torch = _torch()
     Ar, Ai = _dev_planes(M, cplx, torch)
     _native.check(_native.load().hzg_op_cholesky_upper(tw, int(cplx), _p(Ar), _p(Ai), _stream(torch)), None,
                   "matrix is not numerically positive definite")
@@ -88,10 +100,17 @@ def cholesky_upper(M):
 def qr_shorten(Yp, Yq):
     """R factor (nonnegative diagonal) of the stacked block-column pair
     (blocked.py:358-367); RankError on rank deficiency."""
-    torch = _torch()
-    stack = np.hstack([_as_cols(Yp), _as_cols(Yq)])
+    Yp, Yq = _as_cols(Yp), _as_cols(Yq)
+    if Yp.shape[1] != Yq.shape[1]:
+        # the device kernel factors a pair of equal-width block columns
+        # (2w columns); it never truncates to fewer columns
+        raise ValueError("qr_shorten on the device needs block columns of equal width (got %d and %d)"
+                         % (Yp.shape[1], Yq.shape[1]))
+    stack = np.hstack([Yp, Yq])
     cplx = np.iscomplexobj(stack)
     m, tw = stack.shape
+    _check_order(tw, "qr_shorten")
+    torch = _torch()
     Yr, Yi = _dev_planes(stack, cplx, torch)
     Rr = torch.empty((tw, tw), dtype=torch.float64, device=Yr.device)
     Ri = torch.empty((tw, tw), dtype=torch.float64, device=Yr.device) if cplx else None

@@ -152,3 +152,15 @@ def test_product_package_never_uses_the_oracle():
             if pat in text:
                 offenders.append("%s: %s" % (path.name, pat))
     assert not offenders, offenders
+
+
+def test_block_operations_reject_unsupported_shapes():
+    """unsupported or unequal block widths raise a clear
+    ValueError before any device work (no silent truncation)."""
+    from paper_1909_00101_b200 import ops
+    with pytest.raises(ValueError, match="equal width"):
+        ops.qr_shorten(np.ones((8, 2)), np.ones((8, 3)))
+    with pytest.raises(ValueError, match="not supported"):
+        ops.qr_shorten(np.ones((40, 9)), np.ones((40, 9)))
+    with pytest.raises(ValueError, match="not supported"):
+        ops.cholesky_upper(np.eye(3))
