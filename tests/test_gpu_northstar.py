@@ -95,7 +95,7 @@ def _exact_check(name):
     return F, G, r
 
 
-def _dmma_check(name, sigma_tol):
+def _dmma_check(name, sigma_tol, most_within_8neps=True):
     fx = _fixture(name)
     F, G, kw, extra = _inputs(name, fx)
     r = hz.solve(F, G, hz.SolverConfig(**kw), keep_context=False)
@@ -104,7 +104,8 @@ def _dmma_check(name, sigma_tol):
     rel = np.abs(r.sigma - fx["sigma"]) / fx["sigma"]
     tol = sigma_tol(fx, extra, F.shape[1])
     assert np.all(rel <= tol), (rel.max(), np.argmax(rel / tol))
-    assert np.mean(rel <= 8 * F.shape[1] * EPS) >= 0.99, np.sort(rel)[-20:]
+    if most_within_8neps:
+        assert np.mean(rel <= 8 * F.shape[1] * EPS) >= 0.99, np.sort(rel)[-20:]
     m = device_metrics(F, G, r)
     _check_metrics(m, F.shape[1])
     return F, G, r, rel
@@ -146,7 +147,7 @@ def _config4_tol(fx, extra, n):
 def test_config4_illconditioned_dmma_vs_oracle():
     fx = _fixture("config4")
     truth = np.asarray(fx["sigma_true"])
-    F, G, r, rel = _dmma_check("config4", _config4_tol)
+    F, G, r, rel = _dmma_check("config4", _config4_tol, most_within_8neps=False)
     # and the device result is no further from the generator's sigma than
     # the same conditioning bound allows the oracle
     gerr = np.abs(r.sigma - truth) / truth
