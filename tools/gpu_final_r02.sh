@@ -18,3 +18,11 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_p
     -o $out/${tag}_full_w16_n4096 -f python tools/prof_run.py 4096 20 cond 16 > $out/${tag}_f2.log 2>&1
 python tools/ncu_summary.py $out/${tag}_launches_w32_n16384.csv $out/${tag}_launches_w16_n4096.csv \
     $out/${tag}_full_w32_n16384.ncu-rep $out/${tag}_full_w16_n4096.ncu-rep > $out/${tag}_ncu_summary.txt 2>&1
+python tools/ncu_traffic.py $out/${tag}_full_w32_n16384.ncu-rep $out/${tag}_traffic_w32_n16384.json > /dev/null 2>&1
+# the captures stay on the box (gpurun copies back <= 64 MiB): keep the
+# summaries and a source-level table of the inner kernel at n = 4096
+ncu -i $out/${tag}_full_w16_n4096.ncu-rep --page source --csv --print-source cuda,sass -k regex:k_inner \
+    > $out/${tag}_inner_source_w16_n4096.csv 2>/dev/null
+gzip -f $out/${tag}_inner_source_w16_n4096.csv
+rm -f $out/*.ncu-rep
+du -sh $out
