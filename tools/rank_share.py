@@ -9,7 +9,12 @@ shape).  The slowest rank's sweep time bounds the R-GPU sweep from below
 interior groups), so F_sweep / max_r(t_r) estimates strong scaling on R
 B200s where only one GPU is available.
 
-usage: python tools/rank_share.py N R[,R...] [wave|serial|timed|vtimed] [sweeps]
+usage: python tools/rank_share.py N R[,R...] [wave|serial|timed|vtimed|graph] [sweeps] [w]
+
+graph: the library data plane -- the rank's sweep as ONE captured CUDA graph
+(hzg_dist_sweep) on a 1-rank NCCL communicator with its block moves removed
+(they are the only part that needs the other GPUs); host issue is one graph
+launch per sweep.
 """
 import os
 import sys
@@ -36,7 +41,7 @@ def main():
     Rs = [int(x) for x in sys.argv[2].split(",")]
     mode = sys.argv[3] if len(sys.argv) > 3 else "wave"
     nsw = int(sys.argv[4]) if len(sys.argv) > 4 else 2
-    w = 16
+    w = int(sys.argv[5]) if len(sys.argv) > 5 else 16
 
     class A:
         pass
@@ -64,6 +69,36 @@ def main():
             continue
         sched = D.BlockSchedule(n // w, R)
         worst = 0.0
+        if mode == "graph":
+            for r in sorted({0, R // 2, R - 1}):
+                Fw, Gw = F0.clone(), G0.clone()
+                dev = hz.DeviceGsvd({"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}, cfg, epsn=D.epsn_of(cfg, n),
+                                    schedule=sched.colpairs(r, w))
+                dev.comm_attach(1, 0, D.unique_id())
+                dev.comm_set_moves([[] for _ in range(sched.steps)])
+                dev.init()
+                dev.dist_sweep()  # warm-up (graph capture)
+                times, hs = [], []
+                for _ in range(nsw):
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    h0 = time.perf_counter()
+                    dev.dist_sweep()
+                    hs.append(time.perf_counter() - h0)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    times.append(e0.elapsed_time(e1) / 1e3)
+                t = sorted(times)[len(times) // 2]
+                worst = max(worst, t)
+                lo, hi = sched.ranges[r]
+                print(f"n={n} w={w} R={R} rank {r}: {hi - lo} pairs/step, graph: sweep {t * 1e3:.1f} ms "
+                      f"(host wall incl. the sweep's one sync {min(hs) * 1e3:.1f} ms)", flush=True)
+                dev.close()
+                del dev, Fw, Gw
+            print(f"n={n} w={w} R={R} graph: slowest rank {worst * 1e3:.1f} ms/sweep -> "
+                  f"{Fsw / worst / 1e12:.2f} TF/s job, {Fsw / worst / 1e12 / R:.2f} TF/s per GPU", flush=True)
+            continue
         for r in sorted({0, R // 2, R - 1}):
             Fw, Gw = F0.clone(), G0.clone()
             dev = hz.DeviceGsvd({"Fr": Fw, "Gr": Gw, "Fi": None, "Gi": None}, cfg, epsn=D.epsn_of(cfg, n),
