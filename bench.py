@@ -63,8 +63,10 @@ def parse():
     ap.add_argument("--size", dest="n", type=int, default=16384, help="matrix order n (config 5: 16384)")
     ap.add_argument("--kind", default="gauss", choices=["cond", "gauss"],
                     help="gauss: iid Gaussian (config 5); cond: config 4 (sigma in [1e-8, 1e8])")
-    ap.add_argument("--w", type=int, default=32,
-                    help="block width (config 5 default 32: 30 vs 42 sweeps to convergence at n = 16384 with w = 16)")
+    ap.add_argument("--w", type=int, default=None,
+                    help="block width; default 32 on 1-2 GPUs (30 vs 42 sweeps to convergence at n = 16384, "
+                         "67 %% vs 55 %% of the FP64 peak per sweep), 16 on 4+ GPUs (a rank's share of a step is "
+                         "then bound by the inner-solve latency, ~4x longer at 2w = 64; tools/rank_share.py)")
     ap.add_argument("--seed", type=int, default=4096)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--e2e-sweeps", type=int, default=2)
@@ -416,6 +418,8 @@ def config4_full(hz, torch, device, n, w, seed, peak_tflops):
 
 def main():
     a = parse()
+    if a.w is None:
+        a.w = 32 if int(os.environ.get("WORLD_SIZE", "1")) <= 2 else 16
     if a.impl == "reference":
         run_reference(a)
         return

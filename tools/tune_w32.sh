@@ -13,3 +13,5 @@ run HZG_DEFER_Z=0
 run HZG_PRIO=0
 run HZG_INNER_PRIO=1
 run HZG_GROUPS=8
+run HZG_INNER_CTAS=16
+run HZG_INNER_CTAS=24
