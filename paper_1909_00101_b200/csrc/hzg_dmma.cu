@@ -267,7 +267,41 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
   }
   consumer_bar();
   const int g = lane >> 2, t = lane & 3;
-  for (int it = 0; it < ntiles; ++it) {
+  // 2w = 64 real: m16n8k8 MMAs (a quarter of the instructions of m8n8k4 for
+  // the same products; DMMA-bound at this width)
+  constexpr bool M16 = TW == 64 && !CPLX;
+  for (int it = 0; it < ntiles && M16; ++it) {
+    const int s = it % C::NS;
+    mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
+    double* st = stages + s * C::STAGE;
+    double c[C::TN][4];
+#pragma unroll
+    for (int ni = 0; ni < C::TN; ++ni) c[ni][0] = c[ni][1] = c[ni][2] = c[ni][3] = 0.0;
+    const int row = warp * 16 + g;
+#pragma unroll 2
+    for (int k0 = 0; k0 < TW; k0 += 8) {
+      const double a0 = st[(size_t)(k0 + t) * kRS + row], a1 = st[(size_t)(k0 + t) * kRS + row + 8];
+      const double a2 = st[(size_t)(k0 + t + 4) * kRS + row], a3 = st[(size_t)(k0 + t + 4) * kRS + row + 8];
+#pragma unroll
+      for (int ni = 0; ni < C::TN; ++ni) {
+        const int col = ni * 8 + g;
+        dmma1688(c[ni], a0, a1, a2, a3, zs[(size_t)col * C::ZS + k0 + t], zs[(size_t)col * C::ZS + k0 + t + 4]);
+      }
+    }
+    __syncwarp();  // this warp owns its 16 rows: write them back in place
+#pragma unroll
+    for (int ni = 0; ni < C::TN; ++ni) {
+      const int col = ni * 8 + 2 * t;
+      st[(size_t)col * kRS + row] = c[ni][0];
+      st[(size_t)(col + 1) * kRS + row] = c[ni][1];
+      st[(size_t)col * kRS + row + 8] = c[ni][2];
+      st[(size_t)(col + 1) * kRS + row + 8] = c[ni][3];
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[s]);
+  }
+  for (int it = 0; it < ntiles && !M16; ++it) {
     const int s = it % C::NS;
     mbar_wait(&full[s], (uint32_t)((it / C::NS) & 1));
     double* st = stages + s * C::STAGE;

@@ -1056,9 +1056,19 @@ int launch_inner_g(const InnerParams& p, cudaStream_t s) {
   // only allocated when they run: 2w = 64 real then fits 2 CTAs per SM
   using Smem = InnerSmem<TW, CPLX>;
   const size_t full = sizeof(Smem);
-  const size_t smem = p.kc.compensated ? full : offsetof(Smem, cbuf);
+  size_t smem = p.kc.compensated ? full : offsetof(Smem, cbuf);
+  // HZG_INNER_SMEM (KB, performance knob): pad the request so fewer inner
+  // CTAs share an SM and a streaming CTA fits beside one (tuning only)
+  static int pad_kb = -1;
+  if (pad_kb < 0) {
+    const char* e = std::getenv("HZG_INNER_SMEM");
+    pad_kb = e ? std::max(0, std::atoi(e)) : 0;
+  }
+  if ((size_t)pad_kb * 1024 > smem) smem = std::min<size_t>((size_t)pad_kb * 1024, 227 * 1024);
   static PerDeviceOnce attr;
-  if (attr.first()) cudaFuncSetAttribute(k_inner<TW, CPLX, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)full);
+  if (attr.first())
+    cudaFuncSetAttribute(k_inner<TW, CPLX, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(full, smem));
   // HZG_INNER_CTAS caps the CTAs of one launch (each then serves several
   // pairs), leaving SM room for the streaming kernels of other groups
   static int cap = -1;
