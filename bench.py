@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--config4-size", type=int, default=4096, help="full-solve extra of config 4 (0: skip)")
     ap.add_argument("--no-full", action="store_true", help="skip the config-5 full solve + accuracy")
+    ap.add_argument("--no-reference-form", action="store_true",
+                    help="skip the reference-form accuracy report (complete-pivoting LU of Z) of the full solve")
     return ap.parse_args()
 
 
@@ -518,6 +520,18 @@ def main():
                 full["accuracy"] = device_accuracy(torch, Fr0.T, Gr0.T, fout)
                 sig = fout["sigma"]
                 full["sigma_max"], full["sigma_min"] = float(sig[0]), float(sig[-1])
+                if not a.no_reference_form:
+                    # the reference's accuracy_report form (harness.py:436-465):
+                    # X = Z^{-1} by complete-pivoting LU, compensated products
+                    from paper_1909_00101_b200.accuracy import device_accuracy as ref_form
+                    t0 = time.perf_counter()
+                    rf = ref_form((Fr0, None), (Gr0, None), (fout["Ur"], None), (fout["Vr"], None),
+                                  (fout["Zr"], None), fout["sigmaF"], fout["sigmaG"])
+                    full["accuracy_reference_form"] = {
+                        "resF": rf[0], "resG": rf[1], "orthU": rf[2], "orthV": rf[3],
+                        "how": "accuracy_report on the device: X = Z^-1 by LU with complete pivoting "
+                               "(hzg_lu_complete), ||F - U S_F X|| / ||F|| with compensated products",
+                        "seconds": time.perf_counter() - t0}
             del fout
             torch.cuda.empty_cache()
         except Exception as exc:  # the line must still print
