@@ -522,3 +522,23 @@ def test_sweep_graph_repeatable_many_groups(groups, monkeypatch):
             (runs[0].sweeps, runs[0].total_transforms, runs[0].big_transforms)
         for a, b in ((r.sigma, runs[0].sigma), (r.Z.re, runs[0].Z.re), (r.U.re, runs[0].U.re)):
             assert np.array_equal(a, b)
+
+
+def test_solve_keep_context_and_stream_keyed_cache():
+    """solve(keep_context=False) releases the kept device context; a solve
+    under another torch stream builds its own context (the cache key holds
+    the stream) and gives the same bits."""
+    import torch
+    from paper_1909_00101_b200 import solver as S
+    c = load_case("gauss200_w16")
+    cfg = hz.SolverConfig(block_width=16)
+    a = hz.solve(c["F"], c["G"], cfg)
+    assert S._cache["dev"] is not None
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        b = hz.solve(c["F"], c["G"], cfg)
+        assert S._cache["key"][1] == s.cuda_stream
+    assert np.array_equal(a.sigma, b.sigma) and np.array_equal(a.Z.re, b.Z.re)
+    r = hz.solve(c["F"], c["G"], cfg, keep_context=False)
+    assert S._cache["dev"] is None and S._cache["key"] is None
+    assert np.array_equal(r.sigma, a.sigma)
