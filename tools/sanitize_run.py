@@ -29,4 +29,18 @@ print("stripes", r.sweeps)
 os.environ["HZG_FUSED"] = "1"
 r = hz.solve(F, G, hz.SolverConfig(block_width=16, max_outer_sweeps=2, split_rows=256))
 print("fused", r.sweeps)
+os.environ["HZG_FUSED"] = "0"
+r = hz.solve(F, G, hz.SolverConfig(block_width=32, max_outer_sweeps=2))
+print("dmma 2w=64 (m16n8k8 postmultiply)", r.sweeps)
+p = hz.ProblemPair(hz.MatrixPlanePair.from_dense(F[:, :64]), hz.MatrixPlanePair.from_dense(G[:, :64]))
+r = hz.solve(F[:, :64], G[:, :64], hz.SolverConfig(block_width=16))
+print("accuracy report", hz.accuracy_report(p, r))
+from paper_1909_00101_b200 import dist as D  # noqa: E402
+planes, nb, mF, mG = hz.upload_bordered(hz.MatrixPlanePair.from_dense(F), hz.MatrixPlanePair.from_dense(G), 16)
+dev = hz.DeviceGsvd(planes, hz.SolverConfig(block_width=16))
+dev.comm_attach(1, 0, D.unique_id())
+dev.comm_set_moves([[(k % (nb // 16), 0, 0)] for k in range(nb // 16 - 1)])
+dev.init()
+print("nccl rank sweep", dev.dist_sweep())
+dev.close()
 print("sanitize run done")
