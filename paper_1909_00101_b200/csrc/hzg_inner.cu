@@ -869,68 +869,6 @@ k_inner(InnerParams P) {
             store_rows<TW, VEC, RPL, SW>(Zr, di, r0, zi_);
             store_rows<TW, VEC, RPL, SW>(Zr, dj, r0, zj_);
           }
-        } else if (!kc.compensated) {
-          // complex, plain sums: update F and G, decide the sort swap from
-          // the updated F norms (pointwise.py:211-214; every lane takes part
-          // in the shuffles), store F and G, then load, update and store Z
-          // -- Z's rows are never live together with F's and G's
-          bool swap = (flags & 4) != 0;
-          const double z11 = z[0], z12r = z[1], z12i = z[2], z21r = z[3], z21i = z[4], z22 = z[5];
-#define HZG_CUPD(yr, yi, yjr_, yji_)                                                        \
-  {                                                                                        \
-    const double yir = yr[e], yjr = yjr_[e], yii = yi[e], yjI = yji_[e];                   \
-    yr[e] = fma(yjr, z21r, fma(-yjI, z21i, yir * z11));                                    \
-    yi[e] = fma(yjr, z21i, fma(yjI, z21r, yii * z11));                                     \
-    yjr_[e] = fma(yir, z12r, fma(-yii, z12i, yjr * z22));                                  \
-    yji_[e] = fma(yir, z12i, fma(yii, z12r, yjI * z22));                                   \
-  }
-          if (flags & 1) {
-#pragma unroll
-            for (int e = 0; e < RPL; ++e) {
-              HZG_CUPD(fi, fii, fj, fji);
-              HZG_CUPD(gi, gii, gj, gji);
-            }
-          }
-          if (kc.sorting) {
-            double q0[RPL], q1[RPL];
-#pragma unroll
-            for (int e = 0; e < RPL; ++e) {
-              q0[e] = nrm_term<CPLX>(fi[e], fii[e]);
-              q1[e] = nrm_term<CPLX>(fj[e], fji[e]);
-            }
-            double ni = row_tree<RPL>(q0), nj = row_tree<RPL>(q1);
-#pragma unroll
-            for (int d = 1; d < LP; d <<= 1) {
-              ni = ni + __shfl_xor_sync(0xffffffffu, ni, d);
-              nj = nj + __shfl_xor_sync(0xffffffffu, nj, d);
-            }
-            if (flags & 1) swap = ni < nj;
-          }
-          if (flags & 5) {
-            const int di = swap ? j : i, dj = swap ? i : j;
-            store_rows<TW, VEC, RPL, SW>(Ar, di, r0, fi);
-            store_rows<TW, VEC, RPL, SW>(Ar, dj, r0, fj);
-            store_rows<TW, VEC, RPL, SW>(Ai, di, r0, fii);
-            store_rows<TW, VEC, RPL, SW>(Ai, dj, r0, fji);
-            store_rows<TW, VEC, RPL, SW>(Br, di, r0, gi);
-            store_rows<TW, VEC, RPL, SW>(Br, dj, r0, gj);
-            store_rows<TW, VEC, RPL, SW>(Bi, di, r0, gii);
-            store_rows<TW, VEC, RPL, SW>(Bi, dj, r0, gji);
-            double zi_[RPL], zj_[RPL], zii[RPL], zji[RPL];
-            load_rows<TW, VEC, RPL, SW>(Zr, i, r0, zi_);
-            load_rows<TW, VEC, RPL, SW>(Zr, j, r0, zj_);
-            load_rows<TW, VEC, RPL, SW>(Zi, i, r0, zii);
-            load_rows<TW, VEC, RPL, SW>(Zi, j, r0, zji);
-            if (flags & 1) {
-#pragma unroll
-              for (int e = 0; e < RPL; ++e) HZG_CUPD(zi_, zii, zj_, zji);
-            }
-            store_rows<TW, VEC, RPL, SW>(Zr, di, r0, zi_);
-            store_rows<TW, VEC, RPL, SW>(Zr, dj, r0, zj_);
-            store_rows<TW, VEC, RPL, SW>(Zi, di, r0, zii);
-            store_rows<TW, VEC, RPL, SW>(Zi, dj, r0, zji);
-          }
-#undef HZG_CUPD
         } else {
         bool swap = (flags & 4) != 0;
         double zi_[RPL], zj_[RPL], zii[RPL], zji[RPL];
