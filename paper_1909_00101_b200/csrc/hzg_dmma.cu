@@ -229,21 +229,6 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
     fence_mbar_init();
   }
   __syncthreads();
-  // 2w = 64 real: the consumers store their results straight from
-  // registers to global memory, so a stage is free as soon as its MMAs have
-  // read it (no in-place write-back, no bulk store to wait for): the next
-  // tile's load starts one store-drain earlier
-  constexpr bool DIRECT = TW == 64 && !CPLX;
-  if (warp == 4 && DIRECT) {  // producer: loads only
-    for (int it = 0; it < ntiles; ++it) {
-      const int s = it % C::NS;
-      if (it >= C::NS) mbar_wait(&done[s], (uint32_t)(((it / C::NS) - 1) & 1));
-      const int64_t r0 = rbeg + (int64_t)it * kR;
-      const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
-      issue_tile_load<TW, NP>(Y, cp, r0, nv, stages + s * C::STAGE, &full[s], lane);
-    }
-    return;
-  }
   if (warp == 4) {  // producer: loads, and stores of finished tiles
     auto store_tile = [&](int it) {
       const int s = it % C::NS;
@@ -303,28 +288,18 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
         dmma1688(c[ni], a0, a1, a2, a3, zs[(size_t)col * C::ZS + k0 + t], zs[(size_t)col * C::ZS + k0 + t + 4]);
       }
     }
-    // the MMAs have consumed this warp's reads of the stage: release it,
-    // then store the 16 x 64 result rows from registers (rows r0 + row,
-    // r0 + row + 8 of 64 columns; 8 lanes write 8 consecutive rows of one
-    // column, 64 bytes)
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&done[s]);
-    const int64_t r0 = rbeg + (int64_t)it * kR;
-    const int nv = (int)(rend - r0 < kR ? rend - r0 : kR);
+    __syncwarp();  // this warp owns its 16 rows: write them back in place
 #pragma unroll
     for (int ni = 0; ni < C::TN; ++ni) {
       const int col = ni * 8 + 2 * t;
-      double* c0p = Y.re + pair_col(cp, w, col) * Y.ld + r0;
-      double* c1p = Y.re + pair_col(cp, w, col + 1) * Y.ld + r0;
-      if (row < nv) {
-        c0p[row] = c[ni][0];
-        c1p[row] = c[ni][1];
-      }
-      if (row + 8 < nv) {
-        c0p[row + 8] = c[ni][2];
-        c1p[row + 8] = c[ni][3];
-      }
+      st[(size_t)col * kRS + row] = c[ni][0];
+      st[(size_t)(col + 1) * kRS + row] = c[ni][1];
+      st[(size_t)col * kRS + row + 8] = c[ni][2];
+      st[(size_t)(col + 1) * kRS + row + 8] = c[ni][3];
     }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&done[s]);
   }
   for (int it = 0; it < ntiles && !M16; ++it) {
     const int s = it % C::NS;
