@@ -263,6 +263,35 @@ def test_rank_error_on_zero_column():
         hz.solve(F, G, hz.SolverConfig(block_width=4))
 
 
+@pytest.mark.parametrize("exact", [False, True])
+def test_rank_errors_like_the_reference(exact):
+    """The reference raises RankError for a NaN entry, a zero G column and a
+    zero F column of an 8 x 8 random pair (checked against hzgsvd.solve with
+    block_width=2: QR-shortening / prescale rank errors)."""
+    rng = np.random.default_rng(0)
+    cfg = hz.SolverConfig(block_width=2, exact=exact)
+    for spoil in ("nan", "zeroG", "zeroF"):
+        F = rng.standard_normal((8, 8))
+        G = rng.standard_normal((8, 8))
+        if spoil == "nan":
+            F[3, 2] = np.nan
+        elif spoil == "zeroG":
+            G[:, 5] = 0.0
+        else:
+            F[:, 5] = 0.0
+        with pytest.raises(hz.RankError):
+            hz.solve(F, G, cfg)
+
+
+def test_invalid_shapes_raise_value_error():
+    with pytest.raises(ValueError):
+        hz.solve(np.ones((3, 4)), np.ones((4, 4)))  # m_F < n
+    with pytest.raises(ValueError):
+        hz.solve(np.ones((4, 4)), np.ones((4, 3)))  # column counts differ
+    with pytest.raises(ValueError):
+        hz.SolverConfig(variant_id=9)
+
+
 def test_gsvd_blocked_unsorted_and_identity():
     eye = hz.MatrixPlanePair.from_dense(np.eye(16))
     r = hz.gsvd_blocked(hz.ProblemPair(eye, eye), hz.SolverConfig(block_width=4))
