@@ -85,6 +85,12 @@ int hzg_init_fgz(hzg_ctx* ctx);
 /* One outer sweep; returns the sweep's transform counters.  The inter-sweep
  * Z rescale runs on the device when big != 0.  Synchronous. */
 int hzg_sweep(hzg_ctx* ctx, int64_t* total, int64_t* big);
+/* hzg_sweep in two halves: queue the sweep graph and the counter copy on the
+ * bound stream, then wait for them and map the status (several contexts on
+ * different streams -- e.g. the stripe workers of stripes.py -- sweep
+ * concurrently between the two calls). */
+int hzg_sweep_launch(hzg_ctx* ctx);
+int hzg_sweep_wait(hzg_ctx* ctx, int64_t* total, int64_t* big);
 
 /* Run outer steps [first, first + count) of the schedule without the sweep
  * bookkeeping (asynchronous; for profiling and bounded benchmarks). */

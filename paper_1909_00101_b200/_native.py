@@ -24,7 +24,7 @@ class HzgConfig(ctypes.Structure):
                 ("split_rows", ctypes.c_int32), ("approx_2x2", ctypes.c_int32)]
 
 
-EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_set_z_rows", "hzg_init_fgz", "hzg_sweep",
+EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", "hzg_set_z_rows", "hzg_init_fgz", "hzg_sweep", "hzg_sweep_launch", "hzg_sweep_wait",
            "hzg_run_steps", "hzg_run_pairs", "hzg_wave_step", "hzg_wave_join", "hzg_collect", "hzg_rescale_z", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
            "hzg_step_counters", "hzg_debug_phases", "hzg_launch_counts", "hzg_op_grammian",
            "hzg_op_cholesky_upper", "hzg_op_qr_shorten", "hzg_op_qr_rfactor", "hzg_op_postmultiply", "hzg_op_rescale", "hzg_test_fastmath", "hzg_comm_unique_id", "hzg_comm_unique_id_bytes", "hzg_comm_attach",
@@ -60,6 +60,10 @@ def load(path=LIB_PATH):
         L.hzg_init_fgz.argtypes = [P]
         L.hzg_init_fgz.restype = ctypes.c_int
         L.hzg_sweep.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.hzg_sweep_launch.argtypes = [P]
+        L.hzg_sweep_launch.restype = ctypes.c_int
+        L.hzg_sweep_wait.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.hzg_sweep_wait.restype = ctypes.c_int
         L.hzg_sweep.restype = ctypes.c_int
         L.hzg_run_steps.argtypes = [P, I32, I32]
         L.hzg_run_steps.restype = ctypes.c_int

@@ -828,7 +828,7 @@ static int build_graph(hzg_ctx* c) {
   return HZG_OK;
 }
 
-int hzg_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
+int hzg_sweep_launch(hzg_ctx* c) {
   if (!c || !c->bound) return HZG_INVALID;
   cudaError_t e;
   if (!c->gexec) {
@@ -840,6 +840,12 @@ int hzg_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
     return cuda_fail(c, e, "counter copy");
   if ((e = cudaMemcpyAsync(c->h_ctr + 3, c->d_status, 4, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
     return cuda_fail(c, e, "status copy");
+  return HZG_OK;
+}
+
+int hzg_sweep_wait(hzg_ctx* c, int64_t* total, int64_t* big) {
+  if (!c || !c->bound) return HZG_INVALID;
+  cudaError_t e;
   if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "sweep");
   accumulate_times(c);
   if (total) *total = c->h_ctr[0];
@@ -851,6 +857,11 @@ int hzg_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
   std::memcpy(&st, c->h_ctr + 3, 4);
   if (st) return fail(c, HZG_RANK, "zero pencil column between sweeps");
   return HZG_OK;
+}
+
+int hzg_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
+  int rc = hzg_sweep_launch(c);
+  return rc ? rc : hzg_sweep_wait(c, total, big);
 }
 
 int hzg_run_steps(hzg_ctx* c, int32_t first, int32_t count) {

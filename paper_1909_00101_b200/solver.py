@@ -127,6 +127,17 @@ class DeviceGsvd:
         _native.check(self.lib.hzg_sweep(self.ctx, ctypes.byref(tot), ctypes.byref(big)), self.ctx, "sweep")
         return tot.value, big.value
 
+    def sweep_launch(self):
+        """Queue one sweep on the bound stream (returns immediately)."""
+        _native.check(self.lib.hzg_sweep_launch(self.ctx), self.ctx, "sweep")
+
+    def sweep_wait(self):
+        """Wait for the queued sweep: (total, big)."""
+        tot = ctypes.c_int64(0)
+        big = ctypes.c_int64(0)
+        _native.check(self.lib.hzg_sweep_wait(self.ctx, ctypes.byref(tot), ctypes.byref(big)), self.ctx, "sweep")
+        return tot.value, big.value
+
     def run(self, max_sweeps=None):
         """_algorithm1_loop (blocked.py:503-550) with the device doing the work."""
         self.init()

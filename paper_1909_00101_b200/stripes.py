@@ -18,7 +18,9 @@ that scheme so ``workers=s`` is a drop-in:
   with the reference's tag protocol (ProtocolError on a missing or
   duplicate tag, distsim.py:103-144);
 * all s workers live on one GPU here, as the reference's simulation keeps
-  them in one process; each slab's sweep is its own captured CUDA graph.
+  them in one process; each slab's sweep is its own captured CUDA graph on
+  the worker's own stream, and the s sweeps of an outermost step run
+  concurrently (hzg_sweep_launch / hzg_sweep_wait).
 
 In exact mode (SolverConfig(exact=True)) the result is bitwise the
 reference's run_distributed (tests/golden/dist_*.npz).
@@ -172,10 +174,15 @@ class _Worker:
     global rows)."""
 
     def __init__(self, st, cfg, epsn, n):
+        import torch
         from .solver import DeviceGsvd
         self.st = st
         planes = {k: st.storage(k) for k in ("Fr", "Fi", "Gr", "Gi")}
-        self.dev = DeviceGsvd(planes, cfg, epsn=epsn, zrows=n, Z=(st.storage("Zr"), st.storage("Zi")))
+        # every worker's context is bound to its own stream, so the slabs of
+        # one outermost step sweep concurrently on the GPU
+        self.stream = torch.cuda.Stream(device=st.Fr.device)
+        with torch.cuda.stream(self.stream):
+            self.dev = DeviceGsvd(planes, cfg, epsn=epsn, zrows=n, Z=(st.storage("Zr"), st.storage("Zi")))
 
     def init(self):
         """Per-slab prescale (column-local, distsim.py:183-193); the library
@@ -183,31 +190,17 @@ class _Worker:
         row."""
         import torch
         self.dev.init()
-        idx = torch.arange(2 * self.st.width, device=self.dev.device)
-        rows = torch.from_numpy(_logical_rows(self.st)).to(self.dev.device)
-        for key in ("Zr", "Zi"):
-            z = self.st.storage(key)
-            if z is None:
-                continue
-            diag = z[idx, idx].clone()
-            z[idx, idx] = 0.0
-            z[idx, rows] = diag
+        with torch.cuda.stream(self.stream):
+            idx = torch.arange(2 * self.st.width, device=self.dev.device)
+            rows = torch.from_numpy(_logical_rows(self.st)).to(self.dev.device)
+            for key in ("Zr", "Zi"):
+                z = self.st.storage(key)
+                if z is None:
+                    continue
+                diag = z[idx, idx].clone()
+                z[idx, idx] = 0.0
+                z[idx, rows] = diag
 
-    def loop(self, sweep_cap):
-        """_algorithm1_loop(..., sweep_cap, trailing_rescale=True) on the
-        slab: (sweeps, total, big, converged)."""
-        sweeps = total = big = 0
-        converged = False
-        for _ in range(sweep_cap):
-            t, b = self.dev.sweep()  # the inter-sweep rescale is gated on b != 0 in the graph
-            sweeps += 1
-            total += t
-            big += b
-            if b == 0:
-                converged = True
-                break
-        self.dev.rescale_z()
-        return sweeps, total, big, converged
 
     def final(self):
         """Final rescale of the slab: (sigmaF, sigmaG, sigma) device vectors."""
@@ -227,6 +220,35 @@ class _Worker:
 
     def close(self):
         self.dev.close()
+
+
+def _loops(workers, sweep_cap):
+    """_algorithm1_loop(..., sweep_cap, trailing_rescale=True) on every
+    worker's slab (blocked.py:503-550), the workers' sweeps queued together
+    on their streams and waited for together.  Returns the per-worker
+    (total, big) sums."""
+    import torch
+    tot = [0] * len(workers)
+    big = [0] * len(workers)
+    active = list(range(len(workers)))
+    for _ in range(sweep_cap):
+        for q in active:
+            workers[q].dev.sweep_launch()  # the inter-sweep rescale is gated on big != 0 in the graph
+        still = []
+        for q in active:
+            t, b = workers[q].dev.sweep_wait()
+            tot[q] += t
+            big[q] += b
+            if b != 0:
+                still.append(q)
+        active = still
+        if not active:
+            break
+    for wk in workers:
+        wk.dev.rescale_z()  # the trailing rescale
+    torch.cuda.synchronize()  # the stripe exchange reads and writes every slab
+    return tot, big
+
 
 
 def run_distributed(p, cfg=None, s=2, s_inner=1, pool=1):
@@ -249,23 +271,25 @@ def run_distributed(p, cfg=None, s=2, s_inner=1, pool=1):
     table = gen_table(cfg.outer_kind, 2 * s)
     mapping = comm_mapping(table)
     from .solver import _torch
-    _torch()  # no device: fail loudly (no CPU fallback)
+    torch = _torch()  # no device: fail loudly (no CPU fallback)
     states = partition_stripes(p, s, w, cfg.outer_kind, row_multiple=2 * w)
     epsn = cfg.gate_eps * math.sqrt(n)
+    torch.cuda.synchronize()  # slabs built on the current stream, used on the workers' streams
     workers = [_Worker(st, cfg, epsn, n) for st in states]
     try:
         for wk in workers:
             wk.init()
         total = big = sweeps = 0
         converged = False
+        torch.cuda.synchronize()
         for _ in range(OUTERMOST_SWEEPS):
             t_sw = b_sw = 0
             for k in range(len(table.steps)):
-                for wk in workers:
-                    _, t, b, _ = wk.loop(s_inner)
-                    t_sw += t
-                    b_sw += b
+                tot, big_w = _loops(workers, s_inner)
+                t_sw += sum(tot)
+                b_sw += sum(big_w)
                 exchange_step(states, mapping, k)
+                torch.cuda.synchronize()  # the next sweeps run on the workers' streams
             sweeps += 1
             total += t_sw
             big += b_sw
