@@ -230,6 +230,14 @@ int hzg_comm_set_moves(hzg_ctx* ctx, const int32_t* moves, const int32_t* offset
  * count, ncclAllReduce of its status.  Returns the GLOBAL counters; every
  * rank returns the same status.  Synchronous (one host sync per sweep). */
 int hzg_dist_sweep(hzg_ctx* ctx, int64_t* total, int64_t* big);
+/* hzg_dist_sweep in two halves (one process driving several GPUs launches
+ * every rank's sweep graph before waiting for any). */
+int hzg_dist_sweep_launch(hzg_ctx* ctx);
+int hzg_dist_sweep_wait(hzg_ctx* ctx, int64_t* total, int64_t* big);
+/* One process, n GPUs: ncclCommInitAll over the contexts' devices (rank i =
+ * ctxs[i]); the grouped block exchange across them. */
+int hzg_comm_attach_all(hzg_ctx** ctxs, int32_t n);
+int hzg_comm_exchange_all(hzg_ctx** ctxs, int32_t n, const int32_t* moves, int32_t count);
 /* Immediate grouped exchange of whole blocks (e.g. the final gather of
  * every block to rank 0); synchronous. */
 int hzg_comm_exchange(hzg_ctx* ctx, const int32_t* moves, int32_t count);

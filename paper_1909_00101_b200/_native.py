@@ -28,7 +28,8 @@ EXPORTS = ("hzg_create", "hzg_workspace_bytes", "hzg_bind", "hzg_set_schedule", 
            "hzg_run_steps", "hzg_run_pairs", "hzg_wave_step", "hzg_wave_join", "hzg_collect", "hzg_rescale_z", "hzg_finalize", "hzg_test_block", "hzg_set_timing", "hzg_kernel_times",
            "hzg_step_counters", "hzg_debug_phases", "hzg_launch_counts", "hzg_op_grammian",
            "hzg_op_cholesky_upper", "hzg_op_qr_shorten", "hzg_op_qr_rfactor", "hzg_op_postmultiply", "hzg_op_rescale", "hzg_test_fastmath", "hzg_comm_unique_id", "hzg_comm_unique_id_bytes", "hzg_comm_attach",
-           "hzg_comm_set_moves", "hzg_dist_sweep", "hzg_comm_exchange", "hzg_comm_detach", "hzg_lu_workspace_bytes",
+           "hzg_comm_set_moves", "hzg_dist_sweep", "hzg_dist_sweep_launch", "hzg_dist_sweep_wait",
+           "hzg_comm_attach_all", "hzg_comm_exchange_all", "hzg_comm_exchange", "hzg_comm_detach", "hzg_lu_workspace_bytes",
            "hzg_lu_complete", "hzg_gemm_comp", "hzg_sumsq_comp", "hzg_last_error",
            "hzg_destroy")
 
@@ -115,6 +116,14 @@ def load(path=LIB_PATH):
         L.hzg_comm_set_moves.restype = ctypes.c_int
         L.hzg_dist_sweep.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.hzg_dist_sweep.restype = ctypes.c_int
+        L.hzg_dist_sweep_launch.argtypes = [P]
+        L.hzg_dist_sweep_launch.restype = ctypes.c_int
+        L.hzg_dist_sweep_wait.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.hzg_dist_sweep_wait.restype = ctypes.c_int
+        L.hzg_comm_attach_all.argtypes = [P, I32]
+        L.hzg_comm_attach_all.restype = ctypes.c_int
+        L.hzg_comm_exchange_all.argtypes = [P, I32, P, I32]
+        L.hzg_comm_exchange_all.restype = ctypes.c_int
         L.hzg_comm_exchange.argtypes = [P, P, I32]
         L.hzg_comm_exchange.restype = ctypes.c_int
         L.hzg_comm_detach.argtypes = [P]

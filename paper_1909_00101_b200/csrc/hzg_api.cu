@@ -1530,16 +1530,24 @@ static int build_dist_graph(hzg_ctx* c) {
   return HZG_OK;
 }
 
-int hzg_dist_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
+int hzg_dist_sweep_launch(hzg_ctx* c) {
   if (!c || !c->bound || !c->comm) return HZG_INVALID;
   if ((int)c->move_off.size() != c->osteps + 1) return fail(c, HZG_INVALID, "hzg_comm_set_moves first");
   cudaError_t e;
+  if ((e = cudaSetDevice(c->device)) != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
   if (!c->dgexec) {
     if (int rc = build_dist_graph(c)) return rc;
   }
   if ((e = cudaGraphLaunch(c->dgexec, c->stream)) != cudaSuccess) return cuda_fail(c, e, "graph launch");
   if ((e = cudaMemcpyAsync(c->h_ctr, c->d_red, 6 * 8, cudaMemcpyDeviceToHost, c->stream)) != cudaSuccess)
     return cuda_fail(c, e, "counter copy");
+  return HZG_OK;
+}
+
+int hzg_dist_sweep_wait(hzg_ctx* c, int64_t* total, int64_t* big) {
+  if (!c || !c->bound || !c->comm) return HZG_INVALID;
+  cudaError_t e;
+  if ((e = cudaSetDevice(c->device)) != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
   if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return cuda_fail(c, e, "dist sweep");
   ncclResult_t async = ncclSuccess;
   c->nc->CommGetAsyncError(c->comm, &async);
@@ -1551,6 +1559,71 @@ int hzg_dist_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
   if (c->h_ctr[3]) return fail(c, HZG_NOT_PD, "indefinite block Grammian; enable the QR fallback");
   if (c->h_ctr[4]) return fail(c, HZG_RANK, "rank-deficient block pair in the inner solve");
   if (c->h_ctr[5]) return fail(c, HZG_RANK, "zero pencil column between sweeps");
+  return HZG_OK;
+}
+
+int hzg_dist_sweep(hzg_ctx* c, int64_t* total, int64_t* big) {
+  int rc = hzg_dist_sweep_launch(c);
+  return rc ? rc : hzg_dist_sweep_wait(c, total, big);
+}
+
+// One process driving several GPUs: one communicator per context from
+// ncclCommInitAll (rank i = ctxs[i], on ctxs[i]'s device).
+int hzg_comm_attach_all(hzg_ctx** ctxs, int32_t n) {
+  if (!ctxs || n < 1) return HZG_INVALID;
+  std::string err;
+  const hzg::nccl::Api* nc = hzg::nccl::load(err);
+  if (!nc) return HZG_CUDA;
+  std::vector<int> devs(n);
+  std::vector<ncclComm_t> comms(n, nullptr);
+  for (int i = 0; i < n; ++i) {
+    if (!ctxs[i] || ctxs[i]->comm) return HZG_INVALID;
+    devs[i] = ctxs[i]->device;
+  }
+  ncclResult_t r = nc->CommInitAll(comms.data(), n, devs.data());
+  if (r != ncclSuccess) {
+    ctxs[0]->nc = nc;
+    return nccl_fail(ctxs[0], r, "ncclCommInitAll");
+  }
+  for (int i = 0; i < n; ++i) {
+    ctxs[i]->nc = nc;
+    ctxs[i]->comm = comms[i];
+    ctxs[i]->nranks = n;
+    ctxs[i]->rank = i;
+  }
+  return HZG_OK;
+}
+
+// Grouped exchange across the contexts of one process (hzg_comm_attach_all):
+// one NCCL group around every rank's sends and receives, then wait for all.
+int hzg_comm_exchange_all(hzg_ctx** ctxs, int32_t n, const int32_t* moves, int32_t count) {
+  if (!ctxs || n < 1 || count < 0 || (count > 0 && !moves)) return HZG_INVALID;
+  const hzg::nccl::Api* nc = ctxs[0]->nc;
+  if (!nc) return HZG_INVALID;
+  ncclResult_t r = nc->GroupStart();
+  if (r != ncclSuccess) return nccl_fail(ctxs[0], r, "ncclGroupStart");
+  int rc = HZG_OK;
+  for (int i = 0; i < n && rc == HZG_OK; ++i) {
+    hzg_ctx* c = ctxs[i];
+    if (!c || !c->bound || !c->comm) {
+      rc = HZG_INVALID;
+      break;
+    }
+    cudaSetDevice(c->device);
+    std::vector<int32_t> mine;
+    for (int q = 0; q < count; ++q)
+      if (moves[3 * q + 1] == c->rank || moves[3 * q + 2] == c->rank)
+        mine.insert(mine.end(), {moves[3 * q], moves[3 * q + 1], moves[3 * q + 2]});
+    rc = emit_exchange(c, mine.data(), (int)(mine.size() / 3), c->stream);
+  }
+  r = nc->GroupEnd();
+  if (rc) return rc;
+  if (r != ncclSuccess) return nccl_fail(ctxs[0], r, "ncclGroupEnd");
+  for (int i = 0; i < n; ++i) {
+    cudaSetDevice(ctxs[i]->device);
+    cudaError_t e = cudaStreamSynchronize(ctxs[i]->stream);
+    if (e != cudaSuccess) return cuda_fail(ctxs[i], e, "exchange");
+  }
   return HZG_OK;
 }
 

@@ -37,6 +37,7 @@ void do_load() {
     return;
   }
   bool ok = sym(h, "ncclGetUniqueId", g_api.GetUniqueId) && sym(h, "ncclCommInitRank", g_api.CommInitRank) &&
+            sym(h, "ncclCommInitAll", g_api.CommInitAll) &&
             sym(h, "ncclCommDestroy", g_api.CommDestroy) &&
             sym(h, "ncclCommGetAsyncError", g_api.CommGetAsyncError) &&
             sym(h, "ncclGroupStart", g_api.GroupStart) && sym(h, "ncclGroupEnd", g_api.GroupEnd) &&

@@ -327,7 +327,7 @@ class PartitionedGsvd:
     _algorithm1_loop over the partitioned schedule; finalize() gathers the
     blocks to rank 0 and returns its device outputs (None elsewhere)."""
 
-    def __init__(self, planes, cfg, nranks, comm=None, wavefront=True):
+    def __init__(self, planes, cfg, nranks, comm=None, wavefront=True, devices=None):
         import torch
 
         from .solver import DeviceGsvd
@@ -344,7 +344,32 @@ class PartitionedGsvd:
         epsn = epsn_of(cfg, n)
         self.comm = comm
         self.nccl = False
-        if comm is None:
+        self.multi = False
+        if comm == "devices":
+            # one process driving nranks GPUs: a context per
+            # device, ncclCommInitAll, every rank's sweep graph launched
+            # before any is waited for
+            devices = list(range(nranks)) if devices is None else list(devices)
+            if len(devices) != self.nranks:
+                raise ValueError("need one device per rank")
+            self.rank = 0
+            self.devs = []
+            for r, d in enumerate(devices):
+                dd = torch.device("cuda", d)
+                with torch.cuda.device(dd):
+                    pl = {k: (v.to(dd) if v is not None else None) for k, v in planes.items()}
+                    self.devs.append(DeviceGsvd(pl, cfg, device=dd, epsn=epsn, schedule=self.sched.colpairs(r, w)))
+            import ctypes
+            arr = (ctypes.c_void_p * len(self.devs))(*[dv.ctx.value for dv in self.devs])
+            L = _native.load()
+            _native.check(L.hzg_comm_attach_all(arr, len(self.devs)), self.devs[0].ctx, "hzg_comm_attach_all")
+            self._ctx_array = arr
+            for dv in self.devs:
+                dv.comm_set_moves([self.sched.moves(k) for k in range(self.sched.steps)])
+            self.nccl = self.multi = True
+            self.transport = None
+            self.allreduce = None
+        elif comm is None:
             plist = [planes] + [{k: (v.clone() if v is not None else None) for k, v in planes.items()}
                                 for _ in range(self.nranks - 1)]
             self.devs = [DeviceGsvd(plist[r], cfg, epsn=epsn, schedule=self.sched.colpairs(r, w))
@@ -377,7 +402,7 @@ class PartitionedGsvd:
                 dev.comm_attach(world, self.rank, uid[0])
                 dev.comm_set_moves([self.sched.moves(k) for k in range(self.sched.steps)])
                 self.nccl = True
-        ranks = range(self.nranks) if comm is None else [self.rank]
+        ranks = range(self.nranks) if comm in (None, "devices") else [self.rank]
         self.wave = None
         if wavefront and torch.cuda.is_available() and not self.nccl:
             self.wave = Wavefront(self.devs, [self.sched.ranges[r][1] - self.sched.ranges[r][0] for r in ranks],
@@ -397,14 +422,22 @@ class PartitionedGsvd:
         return self
 
     def init(self):
+        import torch
         for d in self.devs:
-            d.init()
+            with torch.cuda.device(d.device):
+                d.init()
         self.sweeps = self.total = self.big = 0
         self.converged = False
 
     def sweep(self):
         """One outer sweep (after init()); returns (total, big)."""
-        if self.nccl:
+        if self.multi:
+            L = _native.load()
+            for d in self.devs:
+                _native.check(L.hzg_dist_sweep_launch(d.ctx), d.ctx, "dist_sweep")
+            res = [d.dist_sweep_wait() for d in self.devs]
+            t, b = res[0]  # every rank holds the same reduced counters
+        elif self.nccl:
             t, b = self.devs[0].dist_sweep()
         else:
             t, b = sweep_ranks(self.devs, self.sched, self.transport, self.allreduce, self.wave)
@@ -415,7 +448,19 @@ class PartitionedGsvd:
         return t, b
 
     def finalize(self, n0=None, mF0=None, mG0=None, sort=True):
-        if self.nccl:
+        import torch
+        with torch.cuda.device(self.devs[0].device):
+            return self._finalize(n0, mF0, mG0, sort)
+
+    def _finalize(self, n0=None, mF0=None, mG0=None, sort=True):
+        if self.multi:
+            moves = gather_blocks(self.sched)
+            arr = np.asarray([x for m in moves for x in m] or [0], dtype=np.int32)
+            import ctypes
+            _native.check(_native.load().hzg_comm_exchange_all(self._ctx_array, len(self.devs),
+                                                              arr.ctypes.data_as(ctypes.c_void_p), len(moves)),
+                          self.devs[0].ctx, "hzg_comm_exchange_all")
+        elif self.nccl:
             self.devs[0].comm_exchange(gather_blocks(self.sched))
         else:
             self.transport.exchange(gather_blocks(self.sched))
@@ -479,11 +524,13 @@ def epsn_of(cfg, n):
     return cfg.gate_eps * math.sqrt(n)
 
 
-def solve_blocks(F, G, cfg, nranks, comm=None, wavefront=True):
+def solve_blocks(F, G, cfg, nranks, comm=None, wavefront=True, devices=None):
     """GSVD of (F, G) with the block-partitioned schedule over nranks ranks.
 
     comm=None: nranks virtual ranks in this process on the current device
-    (block exchange by device copies).  comm="dist": this process is one
+    (block exchange by device copies).  comm="devices": this process drives
+    one GPU per rank (``devices``, default 0..nranks-1) with one NCCL
+    communicator each (ncclCommInitAll).  comm="dist": this process is one
     rank of an initialized torch.distributed job (NCCL, one GPU per rank);
     every rank passes the same F, G and rank 0 returns the result (the
     others return None).  wavefront=False serialises each rank's steps
@@ -503,7 +550,7 @@ def solve_blocks(F, G, cfg, nranks, comm=None, wavefront=True):
     p = ProblemPair(F, G)
     w = cfg.block_width
     planes0, n, mF, mG = upload_bordered(p.F, p.G, w)
-    job = PartitionedGsvd(planes0, cfg, nranks, comm, wavefront=wavefront)
+    job = PartitionedGsvd(planes0, cfg, nranks, comm, wavefront=wavefront, devices=devices)
     try:
         job.run()
         out = job.finalize(p.n, p.F.rows, p.G.rows, sort=True)

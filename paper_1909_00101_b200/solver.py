@@ -180,6 +180,14 @@ class DeviceGsvd:
                       "dist_sweep")
         return tot.value, big.value
 
+    def dist_sweep_wait(self):
+        """Wait for a sweep queued with hzg_dist_sweep_launch: global (total, big)."""
+        tot = ctypes.c_int64(0)
+        big = ctypes.c_int64(0)
+        _native.check(self.lib.hzg_dist_sweep_wait(self.ctx, ctypes.byref(tot), ctypes.byref(big)), self.ctx,
+                      "dist_sweep")
+        return tot.value, big.value
+
     def comm_attach(self, nranks, rank, unique_id):
         """Attach an NCCL communicator (hzg_comm_attach; collective)."""
         buf = ctypes.create_string_buffer(bytes(unique_id), len(unique_id))
@@ -367,7 +375,7 @@ def gsvd_blocked(p, cfg=None, epsn=None):
     return r
 
 
-def solve(F, G, cfg=None, workers=1, worker_sweeps=1, scheme="stripes", keep_context=True):
+def solve(F, G, cfg=None, workers=1, worker_sweeps=1, scheme="stripes", keep_context=True, devices=None):
     """Border, solve on the GPU, unborder, and sort a GSVD problem
     (blocked.py:640-663).
 
@@ -383,8 +391,10 @@ def solve(F, G, cfg=None, workers=1, worker_sweeps=1, scheme="stripes", keep_con
     * "blocks": the B200 block-partitioned schedule (dist.py) -- the
       single-worker ME schedule with its block pairs split over ``workers``
       ranks; bitwise the single-worker result for any rank count (the
-      multi-GPU production path; here the ranks are virtual ranks on the
-      current device, a torchrun job uses dist.solve_blocks).
+      multi-GPU production path; the ranks are virtual ranks on the current
+      device, or -- with ``devices`` -- one GPU each driven from this
+      process with the NCCL exchange inside libhzg; a torchrun job uses
+      dist.solve_blocks(comm="dist")).
 
     ``keep_context`` (single worker): keep the device context (planes,
     workspace, captured sweep graph: about 3.3 n^2 doubles plus the inputs)
@@ -405,8 +415,10 @@ def solve(F, G, cfg=None, workers=1, worker_sweeps=1, scheme="stripes", keep_con
     _native.load()
     if F.cols == 1:
         return gsvd_1x1(F, G)
-    if workers > 1 and scheme == "blocks":
+    if (workers > 1 or devices is not None) and scheme == "blocks":
         from .dist import solve_blocks
+        if devices is not None:  # one process driving one GPU per worker
+            return solve_blocks(F, G, cfg, workers, comm="devices", devices=devices)
         return solve_blocks(F, G, cfg, workers)
     p = ProblemPair(F, G)
     if workers > 1:

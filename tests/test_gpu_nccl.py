@@ -101,3 +101,15 @@ def test_torch_distributed_nccl_world_one_uses_library_plane():
         _same(r, hz.solve(F, G, cfg))
     finally:
         dist.destroy_process_group()
+
+
+def test_one_process_driving_devices_bitwise():
+    """solve(..., scheme="blocks", devices=[...]): one process, one context
+    and ncclCommInitAll communicator per device, every rank's sweep graph
+    launched before any is waited for (hzg_dist_sweep_launch / _wait), the
+    gather by hzg_comm_exchange_all.  With the box's single GPU: devices=[0],
+    bitwise the single-GPU solve."""
+    F, G = _pair(512, 123)
+    cfg = hz.SolverConfig(block_width=16)
+    r = hz.solve(F, G, cfg, workers=1, scheme="blocks", devices=[0])
+    _same(r, hz.solve(F, G, cfg))
