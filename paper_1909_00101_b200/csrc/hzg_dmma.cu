@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(160, (TW == 64 && !CPLX) ? 2 : 1) k_gram_ws(Gr
   if (tid == 0) {
     for (int q = 0; q < C::NS; ++q) {
       mbar_init(&full[q], 1);
-      mbar_init(&empty[q], 4);
+      mbar_init(&empty[q], 128);  // every consumer thread releases the stage it read
     }
     fence_mbar_init();
   }
@@ -162,8 +162,7 @@ __global__ void __launch_bounds__(160, (TW == 64 && !CPLX) ? 2 : 1) k_gram_ws(Gr
           }
         }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    mbar_arrive(&empty[s]);  // each thread's own reads are ordered before its arrive
   }
   consumer_bar();  // every stage consumed: reuse the buffer for the fold
   double* red = stages;
@@ -224,7 +223,7 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
   if (tid == 0) {
     for (int q = 0; q < C::NS; ++q) {
       mbar_init(&full[q], 1);
-      mbar_init(&done[q], 4);
+      mbar_init(&done[q], 128);  // every consumer thread arrives after its own write-back
     }
     fence_mbar_init();
   }
@@ -298,8 +297,7 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
       st[(size_t)(col + 1) * kRS + row + 8] = c[ni][3];
     }
     fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&done[s]);
+    mbar_arrive(&done[s]);
   }
   for (int it = 0; it < ntiles && !M16; ++it) {
     const int s = it % C::NS;
@@ -352,8 +350,7 @@ __global__ void __launch_bounds__(160) k_post_ws(PostParams P) {
           st[(size_t)(p * TW + col + 1) * kRS + row] = acc[p][mi][ni][1];
         }
     fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&done[s]);
+    mbar_arrive(&done[s]);
   }
 }
 
