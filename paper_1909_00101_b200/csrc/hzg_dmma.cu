@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(160) k_postgram(PostGramParams P) {
   if (tid == 0) {
     for (int q = 0; q < C::NS; ++q) {
       mbar_init(&full[q], 1);
-      mbar_init(&done[q], 4);
+      mbar_init(&done[q], 128);  // every consumer thread arrives
     }
     fence_mbar_init();
   }
@@ -548,8 +548,7 @@ __global__ void __launch_bounds__(160) k_postgram(PostGramParams P) {
         }
       }
       fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&done[s]);
+      mbar_arrive(&done[s]);
     }
     if (jn >= 0) {  // fold the warps' partials in k_gram_ws's fixed order
 #pragma unroll
