@@ -1331,6 +1331,16 @@ const char* hzg_last_error(const hzg_ctx* c) { return c ? c->err.c_str() : "null
 // multi-GPU data plane: NCCL inside libhzg
 // ---------------------------------------------------------------------------
 
+// restores the calling thread's current device on scope exit (entry points
+// that switch devices must not change the caller's CUDA state)
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 int hzg_comm_unique_id(void* id_out) {
   if (!id_out) return HZG_INVALID;
   std::string err;
@@ -1350,6 +1360,7 @@ static int nccl_fail(hzg_ctx* c, ncclResult_t r, const char* where) {
 }
 
 int hzg_comm_attach(hzg_ctx* c, int32_t nranks, int32_t rank, const void* unique_id) {
+  DeviceGuard guard;
   if (!c || !unique_id || nranks < 1 || rank < 0 || rank >= nranks) return HZG_INVALID;
   if (c->comm) return fail(c, HZG_INVALID, "communicator already attached");
   std::string err;
@@ -1531,6 +1542,7 @@ static int build_dist_graph(hzg_ctx* c) {
 }
 
 int hzg_dist_sweep_launch(hzg_ctx* c) {
+  DeviceGuard guard;
   if (!c || !c->bound || !c->comm) return HZG_INVALID;
   if ((int)c->move_off.size() != c->osteps + 1) return fail(c, HZG_INVALID, "hzg_comm_set_moves first");
   cudaError_t e;
@@ -1545,6 +1557,7 @@ int hzg_dist_sweep_launch(hzg_ctx* c) {
 }
 
 int hzg_dist_sweep_wait(hzg_ctx* c, int64_t* total, int64_t* big) {
+  DeviceGuard guard;
   if (!c || !c->bound || !c->comm) return HZG_INVALID;
   cudaError_t e;
   if ((e = cudaSetDevice(c->device)) != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
@@ -1597,6 +1610,7 @@ int hzg_comm_attach_all(hzg_ctx** ctxs, int32_t n) {
 // Grouped exchange across the contexts of one process (hzg_comm_attach_all):
 // one NCCL group around every rank's sends and receives, then wait for all.
 int hzg_comm_exchange_all(hzg_ctx** ctxs, int32_t n, const int32_t* moves, int32_t count) {
+  DeviceGuard guard;
   if (!ctxs || n < 1 || count < 0 || (count > 0 && !moves)) return HZG_INVALID;
   const hzg::nccl::Api* nc = ctxs[0]->nc;
   if (!nc) return HZG_INVALID;
