@@ -677,13 +677,14 @@ static int group_cut(int npairs, int G, int g) {
 
 static int choose_groups(const hzg_ctx* c) {
   if (!c->wavefront) return 1;
-  // 8 pairs per group, at most 16 groups (tools/wtime.py, HZG_GROUPS
+  // 4 pairs per group, at most 16 groups (tools/wtime.py, HZG_GROUPS
   // sweep, round 2): config 4 (128 pairs) 8.20 / 8.00 / 7.90 / 7.76 s for
   // 8 / 16 / 32 / 64 groups steady state, 8.77 / 8.51 / 8.99 / 8.87 s on
   // the first call (graph capture + instantiation grow with the groups);
-  // config 3 (64 pairs) 1.31 / 1.25 / 1.20 s for 4 / 8 / 16 groups; n =
+  // config 3 (64 pairs) 1.31 / 1.25 / 1.20 s for 4 / 8 / 16 groups (1.19 s
+  // with this rule); n =
   // 16384, w = 32 (256 pairs) and config 2 within noise for 8 vs 16 / 2-8
-  int g = std::max(1, std::min(16, c->npairs / 8));
+  int g = std::max(1, std::min(16, c->npairs / 4));
   if (const char* e = std::getenv("HZG_GROUPS")) g = std::max(1, std::min(c->npairs, std::atoi(e)));
   return g;
 }
