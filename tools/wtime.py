@@ -12,12 +12,14 @@ import paper_1909_00101_b200 as hz  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
 name = sys.argv[1]
-ws = [int(x) for x in sys.argv[2:]] or [16, 32]
+ws = [int(x) for x in sys.argv[2:] if "=" not in x] or [16, 32]
+# extra SolverConfig fields as key=value (integers), e.g. split_rows=256
+over = {k: int(v) for k, v in (x.split("=") for x in sys.argv[2:] if "=" in x)}
 F, G, kw, extra = O.ns_inputs(name)
 fx = os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "ns_%s.npz" % name)
 ref = dict(np.load(fx)) if os.path.exists(fx) else None
 for w in ws:
-    kw2 = dict(kw, block_width=w)
+    kw2 = dict(kw, block_width=w, **over)
     cfg = hz.SolverConfig(**kw2)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
