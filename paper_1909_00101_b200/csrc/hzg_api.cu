@@ -208,7 +208,7 @@ int cuda_fail(hzg_ctx* c, cudaError_t e, const char* where) {
 // (the fused postmultiply + Grammian needs <= 256); 0 = default geometry.
 // A configuration field, not an environment variable: it sets the
 // Grammians' summation order, i.e. the result bits.
-void gram_split(int64_t m, bool exact, int64_t split_rows_cfg, int& nsplit, int64_t& chunk) {
+void gram_split(int64_t m, bool exact, int64_t split_rows_cfg, int64_t npairs, int& nsplit, int64_t& chunk) {
   const int64_t kSplitRows = split_rows_cfg > 0 ? std::max<int64_t>(64, split_rows_cfg) / 64 * 64 : 0;
   if (exact) {
     int64_t P = pow2c(m);
@@ -221,6 +221,13 @@ void gram_split(int64_t m, bool exact, int64_t split_rows_cfg, int& nsplit, int6
     // never on the GPU count.
     nsplit = kSplitRows > 0 ? (int)pow2c((m + kSplitRows - 1) / kSplitRows)
                             : (int)std::min<int64_t>(8, pow2c((m + 511) / 512));
+    // fewer, longer splits while a step still has >= 1024 Grammian CTAs
+    // (npairs = the problem's pairs per step, not a rank's): fewer partials
+    // to write and for the inner solve to fold (tools/sweep_time.py: n =
+    // 16384, w = 32: 8 -> 2 splits +1.1 %; n = 8192, w = 32: 8 -> 4 +0.9 %;
+    // n = 4096, w = 16 keeps 4+ splits: 2 were 2 % slower)
+    if (kSplitRows == 0)
+      while (nsplit > 1 && npairs * 2 * (nsplit / 2) >= 1024) nsplit /= 2;
     chunk = ((m + nsplit - 1) / nsplit + 63) / 64 * 64;
   }
 }
@@ -510,7 +517,8 @@ int hzg_create(hzg_ctx** out, int device, int64_t mF, int64_t mG, int64_t n, int
   std::vector<int32_t> inner;
   c->isteps = gen_table(cfg->inner_mm != 0, c->tw, inner);
   c->itable_host.assign(inner.begin(), inner.begin() + (size_t)c->isteps * c->tw);
-  for (int mat = 0; mat < 2; ++mat) gram_split(mat == 0 ? mF : mG, !c->use_dmma, cfg->split_rows, c->gw.nsplit[mat], c->gw.chunk[mat]);
+  for (int mat = 0; mat < 2; ++mat)
+    gram_split(mat == 0 ? mF : mG, !c->use_dmma, cfg->split_rows, c->npairs, c->gw.nsplit[mat], c->gw.chunk[mat]);
   if (c->comp) {  // the compensated Grammian is one sequential form over the full height
     c->gw.nsplit[0] = c->gw.nsplit[1] = 1;
     c->gw.chunk[0] = mF;
@@ -1227,7 +1235,7 @@ int hzg_op_grammian(int64_t m, int32_t w, int32_t cplx, int32_t comp, const doub
   GramWS gw{};
   int nsplit = 1;
   int64_t chunk = m;
-  if (!comp) gram_split(m, true, 0, nsplit, chunk);
+  if (!comp) gram_split(m, true, 0, 0, nsplit, chunk);
   gw.nsplit[0] = gw.nsplit[1] = nsplit;
   gw.chunk[0] = gw.chunk[1] = chunk;
   gw.smax = nsplit;
