@@ -504,6 +504,51 @@ def test_pivot_property_many_random_2x2(cplx):
 
 
 @pytest.mark.parametrize("cplx", [False, True])
+def test_short_chain_2x2_diagonalization_property(cplx):
+    """The reference's kernel property suite (test_acceptance.py:267-290,
+    test_kernel2x2.py:167-203) on the device's short-chain 2x2 forms (DMMA
+    mode, approx_2x2): over 10^4 random pivots (2w = 2, one pivot per block,
+    4-row columns as the reference draws them), the block solve's Z~ makes
+    both Grammians diagonal -- off-diagonal / sqrt(diagonal product) <= 64
+    ulp / t^2, t^2 = 1 - cos^2(g_1, g_2) (the transform's conditioning) --
+    with det Z~ != 0; pivots the gate leaves alone are skipped as the
+    reference skips relatively orthogonal ones."""
+    rng = np.random.default_rng(424242 + cplx)
+    cfg = hz.SolverConfig(block_width=1)
+    assert cfg.approx_2x2 and not cfg.exact
+    epsn = EPS * np.sqrt(2.0)
+    worst_a = worst_b = 0.0
+    tested = 0
+    for t in range(10000):
+        Y = rng.standard_normal((4, 2)) + (1j * rng.standard_normal((4, 2)) if cplx else 0)
+        X = rng.standard_normal((4, 2)) + (1j * rng.standard_normal((4, 2)) if cplx else 0)
+        grams = []
+        for M in (Y, X):
+            Ar, Ai = O.grammian(np.asfortranarray(M.real), np.asfortranarray(M.imag) if cplx else None, 0, 1, 1,
+                                cplx)
+            grams.append((Ar, Ai))
+        A = grams[0][0] + (1j * grams[0][1] if cplx else 0)
+        B = grams[1][0] + (1j * grams[1][1] if cplx else 0)
+        cos2 = abs(B[0, 1]) ** 2 / (B[0, 0].real * B[1, 1].real)
+        if abs(A[0, 1]) < np.sqrt(A[0, 0].real * A[1, 1].real) * epsn and np.sqrt(cos2) < epsn:
+            continue
+        Zg, cnt = _gpu_block(2, cplx, cfg, epsn, grams)
+        assert cnt[2] == 0 and cnt[0] >= 1, t
+        t2 = 1.0 - cos2
+        for M, acc in ((A, "a"), (B, "b")):
+            D = Zg.conj().T @ M @ Zg
+            d = abs(D[0, 1]) / np.sqrt(D[0, 0].real * D[1, 1].real) * t2
+            if acc == "a":
+                worst_a = max(worst_a, d)
+            else:
+                worst_b = max(worst_b, d)
+        assert abs(np.linalg.det(Zg)) > 0.0, t
+        tested += 1
+    assert tested > 9000
+    assert worst_a <= 64 * EPS and worst_b <= 64 * EPS, (worst_a / EPS, worst_b / EPS)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
 def test_sigma_vs_numpy_svd_of_F_Ginv(cplx):
     """sigma against numpy's SVD of F G^-1 at n = 24 (test_blocked.py:263-273),
     with the reference's tolerance 1e-10."""

@@ -1,5 +1,5 @@
 """Where the time of one end-to-end solve() goes (the bench's e2e call:
-pinned numpy inputs, max_outer_sweeps=2): python tools/e2e_breakdown.py [n]"""
+pinned numpy inputs, max_outer_sweeps=2): python tools/e2e_breakdown.py [n] [w]"""
 import os
 import sys
 import time
@@ -12,6 +12,7 @@ import paper_1909_00101_b200 as hz
 from paper_1909_00101_b200 import solver as S
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+w = int(sys.argv[2]) if len(sys.argv) > 2 else 32
 
 
 class A:
@@ -19,14 +20,14 @@ class A:
 
 
 a = A()
-a.n, a.kind, a.seed, a.w = n, "gauss", 7, 16
+a.n, a.kind, a.seed, a.w = n, "gauss", 7, w
 F0, G0, _ = bench.gen_pair(a, torch, torch.device("cuda"))
 Fh = torch.empty(F0.shape, dtype=torch.float64, pin_memory=True)
 Gh = torch.empty(G0.shape, dtype=torch.float64, pin_memory=True)
 Fh.copy_(F0)
 Gh.copy_(G0)
 Fnp, Gnp = Fh.numpy().T, Gh.numpy().T
-cfg = hz.SolverConfig(block_width=16, max_outer_sweeps=2)
+cfg = hz.SolverConfig(block_width=w, max_outer_sweeps=2)
 hz.solve(Fnp, Gnp, cfg)
 for rep in range(2):
     T = {}
