@@ -304,6 +304,95 @@ __device__ int warp_cholesky(double* Ar, double* Ai, int lane) {
 #undef AI_
 }
 
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// warp_cholesky by NTH threads (a named barrier `bar` of its own, so the F
+// and G factorizations run side by side): the same operations in the same
+// per-element order -- element (x, jp) of the trailing triangle is updated
+// by the columns j < jp in ascending order -- so the factor is bitwise
+// warp_cholesky's.  Thread (tx, ty) owns rows x = tx (mod TX) and the
+// columns jp = ty (mod TY) of them; each column step is scale | barrier |
+// update | barrier, the update in chunks of four independent elements
+// (loads before stores: no shared-memory aliasing stalls).
+template <int TW, bool CPLX, int SW, int NTH>
+__device__ int group_cholesky(double* Ar, double* Ai, int t, int bar) {
+#define A_(x, y) Ar[(y) * TW + rp<SW, TW>(x)]
+#define AI_(x, y) Ai[(y) * TW + rp<SW, TW>(x)]
+  constexpr int TX = TW < NTH ? TW : NTH;
+  constexpr int TY = NTH / TX;
+  static_assert(NTH % TX == 0, "thread grid");
+  const int tx = t % TX, ty = t / TX;
+  for (int j = 0; j < TW; ++j) {
+    const double d = A_(j, j);
+    if (!(d > 0.0) || !isfinite(d)) return 1;  // every thread read the same d
+    const double rt = sqrt(d);
+    const double rinv = 1.0 / rt;
+    if (ty == 0)
+      for (int x = tx; x < TW; x += TX)
+        if (x > j) {
+          A_(x, j) *= rinv;
+          if (CPLX) AI_(x, j) *= rinv;
+        }
+    named_bar(bar, NTH);
+    for (int x = tx; x < TW; x += TX) {
+      if (x < j) continue;
+      if (x == j) {  // nobody reads the diagonal during the update
+        if (ty == 0) {
+          A_(j, j) = rt;
+          if (CPLX) AI_(j, j) = 0.0;
+        }
+        continue;
+      }
+      const double ar = -A_(x, j);
+      const double ai = CPLX ? -AI_(x, j) : 0.0;
+      int jp = j + 1 + (((ty - (j + 1)) % TY) + TY) % TY;
+      for (; jp + 3 * TY <= x; jp += 4 * TY) {
+        double br[4], bi[4], cr[4], ci[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          br[q] = A_(jp + q * TY, j);
+          bi[q] = CPLX ? -AI_(jp + q * TY, j) : 0.0;
+          cr[q] = A_(x, jp + q * TY);
+          ci[q] = CPLX ? AI_(x, jp + q * TY) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (CPLX) {
+            A_(x, jp + q * TY) = fma(ar, br[q], fma(-ai, bi[q], cr[q]));
+            AI_(x, jp + q * TY) = fma(ar, bi[q], fma(ai, br[q], ci[q]));
+          } else {
+            A_(x, jp + q * TY) = fma(ar, br[q], cr[q]);
+          }
+        }
+      }
+      for (; jp <= x; jp += TY) {
+        const double br = A_(jp, j);
+        if (CPLX) {
+          const double bi = -AI_(jp, j);
+          A_(x, jp) = fma(ar, br, fma(-ai, bi, A_(x, jp)));
+          AI_(x, jp) = fma(ar, bi, fma(ai, br, AI_(x, jp)));
+        } else {
+          A_(x, jp) = fma(ar, br, A_(x, jp));
+        }
+      }
+    }
+    named_bar(bar, NTH);
+  }
+  // conj-transpose into the upper triangle, zero the strict lower one
+  for (int r = t; r < TW; r += NTH)
+    for (int c = 0; c < r; ++c) {
+      A_(c, r) = A_(r, c);
+      if (CPLX) AI_(c, r) = -AI_(r, c);
+      A_(r, c) = 0.0;
+      if (CPLX) AI_(r, c) = 0.0;
+    }
+  return 0;
+#undef A_
+#undef AI_
+}
+
 // Householder R factor of the m x TW block-column stack (blocked.py:97-217
 // with pivot=False, via _shorten_qr :487-500), bitwise in the reference's
 // sequential fma order.  Sequential chains over m make this slow; it only
@@ -550,8 +639,18 @@ k_inner(InnerParams P) {
   }
   __syncthreads();
 
-  // ---- Cholesky of both Grammians (warp 0: F, warp 1: G) -----------------
-  if (warp < 2 && !kc.shorten_qr) {
+  // ---- Cholesky of both Grammians -----------------------------------------
+  // (2+ warps: the first half of the CTA factors F, the second G)
+  if constexpr (NW >= 2 && NW % 2 == 0) {
+    if (!kc.shorten_qr) {
+      constexpr int NTH = NW * 16;
+      const int half = tid / NTH;
+      double* Mr = half == 0 ? S.A[0] : S.B[0];
+      double* Mi = CPLX ? (half == 0 ? S.A[NP - 1] : S.B[NP - 1]) : nullptr;
+      const int f = group_cholesky<TW, CPLX, SW, NTH>(Mr, Mi, tid % NTH, 1 + half);
+      if (tid % NTH == 0) S.chol_fail[half] = f;
+    }
+  } else if (warp < 2 && !kc.shorten_qr) {
     double* Mr = warp == 0 ? S.A[0] : S.B[0];
     double* Mi = CPLX ? (warp == 0 ? S.A[NP - 1] : S.B[NP - 1]) : nullptr;
     int f = warp_cholesky<TW, CPLX, SW>(Mr, Mi, lane);

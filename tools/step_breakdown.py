@@ -49,3 +49,23 @@ for sw in range(100):
         show("sweep %d" % (sw + 1), kt)
     if b == 0:
         break
+
+# the converged regime: inner-step cycles of CTA 0 (hzg_debug_phases) over
+# one more sweep, against the inner launch time
+import ctypes  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ph = np.zeros(4, dtype=np.int64)
+dev.lib.hzg_debug_phases(dev.ctx, 1, None)
+kt, b = timed_sweep()
+dev.lib.hzg_debug_phases(dev.ctx, 0, ph.ctypes.data_as(ctypes.c_void_p))
+ph[0] -= (int(ph[0]) // 1000000000) * 1000000000
+show("one more sweep (phase counters on)", kt)
+steps = int(ph[3])
+cyc = ph[:3].sum() / max(1, steps)
+inner_us = kt["inner"][0] * 1e3 / osteps
+loop_us = steps / osteps * cyc / 1.965e3
+print("CTA 0: %.1f inner steps per outer step, %.0f cycles each (A %.0f B %.0f C %.0f): %.1f us of the %.1f us "
+      "inner launch; the rest (fold, Cholesky, prescale, theta rescale, identity test, Z~ store, launch) %.1f us"
+      % (steps / osteps, cyc, ph[0] / steps, ph[1] / steps, ph[2] / steps, loop_us, inner_us, inner_us - loop_us))
