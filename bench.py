@@ -636,7 +636,7 @@ def main():
 
     extra = None
     if world == 1 and a.config4_size > 0:
-        # config 4 at w = 16: 8.3 s vs 8.5 s at w = 32 (inner-solve bound at n = 4096)
+        # config 4 at w = 16: 7.8 s vs 8.5 s at w = 32 and no convergence in 100 sweeps at w = 8 (tools/wtime.py)
         extra = config4_full(hz, torch, device, a.config4_size, 16, 4096, peak_tf)
 
     cpu = None
